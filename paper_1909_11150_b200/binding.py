@@ -1,0 +1,208 @@
+"""Thin ctypes binding over libgr.so (include/gr.h). Argument marshalling only:
+every step of the method runs in the library's sm_100a kernels. The functions
+keep the C names (gr_init, gr_mark_ready, gr_step, gr_wait, ...).
+
+There is no fallback: if libgr.so is missing or fails to load, importing this
+module raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libgr.so")
+
+GR_OK, GR_EINVAL, GR_ESTATE, GR_EMISMATCH, GR_ECUDA, GR_ETIMEOUT, GR_EABORT, GR_ESHUTDOWN, GR_ENOMEM = \
+    0, -1, -2, -3, -4, -5, -6, -7, -8
+STATUS_NAMES = {0: "GR_OK", -1: "GR_EINVAL", -2: "GR_ESTATE", -3: "GR_EMISMATCH", -4: "GR_ECUDA",
+                -5: "GR_ETIMEOUT", -6: "GR_EABORT", -7: "GR_ESHUTDOWN", -8: "GR_ENOMEM"}
+GR_F32, GR_F16 = 0, 1
+GR_Q_WORDS, GR_Q_BIT_OF, GR_Q_BUF_OFFSET, GR_Q_NCHUNKS, GR_Q_STATS, GR_Q_LAST_ALGO = range(6)
+GR_ALGO_NONE, GR_ALGO_LOCAL, GR_ALGO_ONESHOT, GR_ALGO_TWOSHOT = range(4)
+
+ALLGATHER_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p)
+
+
+class GrWorld(ctypes.Structure):
+    _fields_ = [("rank", ctypes.c_int32), ("world_size", ctypes.c_int32), ("device", ctypes.c_int32),
+                ("compute_stream", ctypes.c_void_p), ("buffer_dtype", ctypes.c_int),
+                ("one_shot_max_bytes", ctypes.c_int64), ("timeout_ms", ctypes.c_int32),
+                ("comm_ctas", ctypes.c_int32), ("chunk_elems", ctypes.c_int64),
+                ("allgather", ALLGATHER_FN), ("user", ctypes.c_void_p)]
+
+
+class GrTensor(ctypes.Structure):
+    _fields_ = [("numel", ctypes.c_int64), ("grad_dtype", ctypes.c_int)]
+
+
+class GrCycleInfo(ctypes.Structure):
+    _fields_ = [("n_released", ctypes.c_int32), ("step_complete", ctypes.c_int32), ("cycle", ctypes.c_int64),
+                ("step", ctypes.c_int64), ("released_elems", ctypes.c_int64)]
+
+
+class GrStats(ctypes.Structure):
+    _fields_ = [("cycles", ctypes.c_int64), ("steps", ctypes.c_int64), ("bitvector_launches", ctypes.c_int64),
+                ("data_launches", ctypes.c_int64), ("released_elems", ctypes.c_int64),
+                ("data_kernel_ms", ctypes.c_double), ("bitvector_kernel_ms", ctypes.c_double)]
+
+
+class GrError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"{STATUS_NAMES.get(code, code)}: {msg}")
+        self.code = code
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is missing: run `python -c 'import __graft_entry__ as g; g.build()'` "
+                          "(there is no CPU fallback)")
+    L = ctypes.CDLL(LIB_PATH)
+    p, i32, i64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64
+    sig = {
+        "gr_init": ([ctypes.POINTER(p), ctypes.POINTER(GrWorld), ctypes.POINTER(GrTensor), i32, p, i32], ctypes.c_int),
+        "gr_mark_ready": ([p, i32, i32, p], ctypes.c_int),
+        "gr_mark_ready_async": ([p, i32, i32, p, p], ctypes.c_int),
+        "gr_step": ([p, p, ctypes.POINTER(GrCycleInfo), p], ctypes.c_int),
+        "gr_wait": ([p], ctypes.c_int),
+        "gr_set_status": ([p, i32, i32], ctypes.c_int),
+        "gr_finalize": ([p], ctypes.c_int),
+        "gr_last_error": ([p], ctypes.c_char_p),
+        "gr_query": ([p, i32, p, ctypes.c_size_t], ctypes.c_int),
+        "gr_set_timing": ([p, i32], ctypes.c_int),
+        "gr_reset_stats": ([p], ctypes.c_int),
+        "gr_bench_spin": ([i64, i32, p], ctypes.c_int),
+    }
+    for name, (args, res) in sig.items():
+        f = getattr(L, name)
+        f.argtypes = args
+        f.restype = res
+    return L
+
+
+lib = _load()
+EXPORTED = ("gr_init", "gr_mark_ready", "gr_mark_ready_async", "gr_step", "gr_wait", "gr_set_status",
+            "gr_finalize", "gr_last_error", "gr_query", "gr_set_timing", "gr_reset_stats", "gr_bench_spin")
+
+
+def _check(rc: int, ctx=None):
+    if rc != GR_OK:
+        raise GrError(rc, lib.gr_last_error(ctx).decode())
+    return rc
+
+
+def make_allgather(pg=None, device=None):
+    """Allgather callback over torch.distributed (gloo: CPU tensors, nccl: CUDA tensors)."""
+    import torch
+    import torch.distributed as dist
+
+    def cb(send, recv, nbytes, _user):
+        try:
+            ws = dist.get_world_size(pg)
+            backend = dist.get_backend(pg)
+            dev = torch.device("cuda", device) if (backend == "nccl" and device is not None) else \
+                (torch.device("cuda", torch.cuda.current_device()) if backend == "nccl" else torch.device("cpu"))
+            src = torch.frombuffer(ctypes.string_at(send, nbytes), dtype=torch.uint8).to(dev)
+            out = torch.empty(ws * nbytes, dtype=torch.uint8, device=dev)
+            dist.all_gather_into_tensor(out, src, group=pg)
+            data = out.cpu().numpy().tobytes()
+            ctypes.memmove(recv, data, len(data))
+            return 0
+        except Exception as e:  # never raise through the C frame
+            print(f"[gr allgather] {e!r}")
+            return 1
+
+    return ALLGATHER_FN(cb)
+
+
+class Context:
+    """Owns one gr_ctx; methods map 1:1 onto the C calls."""
+
+    def __init__(self, *, rank: int, world_size: int, device: int, numel, group_of, grad_f16=None,
+                 buffer_dtype: int = GR_F16, compute_stream: int = 0, one_shot_max_bytes: int = -1,
+                 timeout_ms: int = 0, comm_ctas: int = 0, chunk_elems: int = 0, allgather=None):
+        T = len(numel)
+        self.T = T
+        self.G = int(max(group_of)) + 1
+        tab = (GrTensor * T)()
+        for t in range(T):
+            tab[t].numel = int(numel[t])
+            tab[t].grad_dtype = GR_F16 if (grad_f16 is not None and grad_f16[t]) else GR_F32
+        grp = (ctypes.c_int32 * T)(*[int(g) for g in group_of])
+        self._allgather = allgather if allgather is not None else ALLGATHER_FN()
+        w = GrWorld(rank, world_size, device, compute_stream, buffer_dtype, one_shot_max_bytes, timeout_ms,
+                    comm_ctas, chunk_elems, self._allgather, None)
+        self._ctx = ctypes.c_void_p()
+        rc = lib.gr_init(ctypes.byref(self._ctx), ctypes.byref(w), tab, T, ctypes.cast(grp, ctypes.c_void_p), self.G)
+        _check(rc, None)
+        self.rank = rank
+        self.W = self.query_int(GR_Q_WORDS)
+        self._released = (ctypes.c_int32 * self.G)()
+        self._bits = (ctypes.c_uint32 * self.W)()
+        self._info = GrCycleInfo()
+
+    # -- the four calls of the method ------------------------------------------------------
+    def gr_mark_ready(self, tensor_id: int, dev_ptr: int, rank: int | None = None):
+        return _check(lib.gr_mark_ready(self._ctx, self.rank if rank is None else rank, tensor_id, dev_ptr), self._ctx)
+
+    def gr_mark_ready_async(self, tensor_id: int, dev_ptr: int, stream: int, rank: int | None = None):
+        return _check(lib.gr_mark_ready_async(self._ctx, self.rank if rank is None else rank, tensor_id, dev_ptr,
+                                              stream), self._ctx)
+
+    def gr_step(self):
+        """Returns (released group ids, step_complete, A words (list of int), info)."""
+        _check(lib.gr_step(self._ctx, ctypes.cast(self._released, ctypes.c_void_p), ctypes.byref(self._info),
+                           ctypes.cast(self._bits, ctypes.c_void_p)), self._ctx)
+        n = self._info.n_released
+        return list(self._released[:n]), bool(self._info.step_complete), list(self._bits), self._info
+
+    def gr_wait(self):
+        return _check(lib.gr_wait(self._ctx), self._ctx)
+
+    # -- extras ------------------------------------------------------------------------------
+    def gr_set_status(self, abort: bool = False, shutdown: bool = False):
+        return _check(lib.gr_set_status(self._ctx, int(abort), int(shutdown)), self._ctx)
+
+    def query_int(self, kind: int) -> int:
+        v = ctypes.c_int32()
+        _check(lib.gr_query(self._ctx, kind, ctypes.byref(v), 4), self._ctx)
+        return v.value
+
+    def bit_of(self):
+        a = (ctypes.c_int32 * self.T)()
+        _check(lib.gr_query(self._ctx, GR_Q_BIT_OF, a, 4 * self.T), self._ctx)
+        return list(a)
+
+    def buf_offsets(self):
+        a = (ctypes.c_int64 * self.T)()
+        _check(lib.gr_query(self._ctx, GR_Q_BUF_OFFSET, a, 8 * self.T), self._ctx)
+        return list(a)
+
+    def stats(self) -> GrStats:
+        s = GrStats()
+        _check(lib.gr_query(self._ctx, GR_Q_STATS, ctypes.byref(s), ctypes.sizeof(s)), self._ctx)
+        return s
+
+    def set_timing(self, on: bool):
+        _check(lib.gr_set_timing(self._ctx, int(on)), self._ctx)
+
+    def reset_stats(self):
+        _check(lib.gr_reset_stats(self._ctx), self._ctx)
+
+    def last_error(self) -> str:
+        return lib.gr_last_error(self._ctx).decode()
+
+    def gr_finalize(self):
+        if self._ctx:
+            lib.gr_finalize(self._ctx)
+            self._ctx = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.gr_finalize()
+        except Exception:
+            pass
+
+
+def gr_bench_spin(ns: int, ctas: int, stream: int):
+    return _check(lib.gr_bench_spin(int(ns), int(ctas), stream))

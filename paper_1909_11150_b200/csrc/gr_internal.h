@@ -1,0 +1,99 @@
+// gr_internal.h — shared between the host runtime (gr_runtime.cpp) and the
+// sm_100a kernels (gr_kernels.cu). Not part of the ABI (include/gr.h is).
+#pragma once
+#include <cstdint>
+
+#define GR_MAX_RANKS 8
+#define GR_STATUS_BITS 2
+#define GR_SLOT_RING 64            // released-list slots in flight (cycle % ring)
+
+namespace gr {
+
+// One piece of one tensor inside one chunk of the static fusion layout.
+struct Seg {
+    int32_t tensor;      // tensor id
+    int32_t grad_f16;    // 1 if the caller's gradient is fp16
+    int64_t tensor_off;  // element offset inside the tensor (multiple of 8)
+    int64_t buf_off;     // element offset inside the fusion buffer (multiple of 8)
+    int64_t len;         // elements
+};
+
+// A chunk: contiguous fusion-buffer range of one group, cut at chunk_elems.
+struct Chunk {
+    int32_t seg_begin, seg_end;
+};
+
+// Written by the bitvector kernel into pinned host-mapped memory; the host
+// polls `seq`. Followed in memory by A[W] (u32) and released[G] (i32).
+struct HostResult {
+    volatile uint64_t seq;
+    int32_t status;          // 0 ok, 1 abort, 2 shutdown, 3 timeout
+    int32_t n_released;
+    int32_t step_complete;
+    int32_t total_chunks;
+    int64_t released_elems;
+};
+
+struct HostError {
+    volatile int32_t code;   // 0 none, 3 timeout in the data kernel
+    volatile int32_t where;
+};
+
+enum { ST_OK = 0, ST_ABORT = 1, ST_SHUTDOWN = 2, ST_TIMEOUT = 3 };
+
+struct BvParams {
+    const uint32_t *host_bits;       // host-mapped [W]: bits set by gr_mark_ready (cleared per step)
+    const uint32_t *dev_flags;       // device [W*32]: step epoch written by gr_mark_ready_async
+    const uint64_t *host_ptr;        // host-mapped [T]
+    uint64_t *dev_ptr;               // device [T]
+    uint32_t *ptr_epoch;             // device [T]: epoch whose pointer dev_ptr holds
+    const int32_t *tensor_of_bit;    // device [nbits]
+    const int32_t *group_of_bit;     // device [nbits]
+    const int32_t *group_bit_begin;  // device [G]
+    const int32_t *group_bit_end;    // device [G]
+    const int32_t *group_nchunks;    // device [G]
+    const int64_t *group_elems;      // device [G]
+    uint32_t *group_rel_epoch;       // device [G]: epoch in which the group was released
+    uint64_t *slot[GR_MAX_RANKS];    // every rank's LL bitvector slots [2][W] (own = local)
+    int32_t *out_released;           // device [G]   (ring slot)
+    int32_t *out_cum;                // device [G+1] (ring slot)
+    HostResult *result;              // host-mapped
+    int32_t T, G, W, nbits, rank, N;
+    uint32_t epoch;                  // training-step epoch (>= 1)
+    uint32_t tag;                    // cycle tag written into each LL word (!= 0)
+    int32_t parity;                  // cycle & 1
+    int32_t abort_flag, shutdown_flag;
+    uint64_t timeout_ns;
+    uint64_t seq;
+};
+
+enum Algo { ALGO_LOCAL = 1, ALGO_ONESHOT = 2, ALGO_TWOSHOT = 3 };
+
+struct DataParams {
+    const Seg *segs;
+    const Chunk *chunks;
+    const int32_t *group_chunk_begin;  // [G]
+    const int32_t *released;           // ring slot [G]
+    const int32_t *cum;                // ring slot [G+1]
+    const uint64_t *dev_ptr;           // [T]
+    char *buf[GR_MAX_RANKS];           // every rank's fusion buffer for this step parity
+    uint32_t *pack_flag[GR_MAX_RANKS]; // every rank's pack flags [C][N] for this parity
+    uint32_t *rs_flag[GR_MAX_RANKS];   // every rank's reduce-scatter flags [C] for this parity
+    int32_t *work_counter;             // device, reset by the last CTA
+    int32_t *done_counter;
+    volatile int32_t *abort_dev;       // device flag: bail out (set on timeout)
+    HostError *err;                    // host-mapped
+    int32_t n_released, total_chunks;
+    int32_t rank, N;
+    uint32_t epoch;
+    float inv_n;
+    uint64_t timeout_ns;
+};
+
+// Kernel launchers (gr_kernels.cu). Return cudaError_t as int.
+int launch_bitvector(const BvParams &p, void *stream);
+int launch_data(const DataParams &p, int algo, int buffer_f16, int ctas, void *stream);
+int data_kernel_max_ctas(int algo, int buffer_f16, int *out);
+int launch_spin(int64_t ns, int ctas, void *stream);
+
+}  // namespace gr

@@ -1,0 +1,786 @@
+// gr_runtime.cpp — host runtime behind include/gr.h.
+//
+// Owns: the response cache (static bit positions, "processed by
+// the coordinator rank only once ... stored in a cache on every worker"), the
+// static group-major fusion layout and its chunk/segment tables, the
+// symmetric memory mapped into every peer with CUDA IPC, the pinned
+// host-mapped ready flags / pointer table / result block, the two streams
+// (coordination, data), the cycle / step epochs and the error state.
+// All arithmetic of the method runs in gr_kernels.cu.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "gr.h"
+#include "gr_internal.h"
+
+using gr::Chunk;
+using gr::Seg;
+
+namespace {
+
+thread_local std::string g_init_error = "no error";
+
+constexpr int64_t kDefaultChunkElems = 32768;
+constexpr int32_t kDefaultTimeoutMs = 20000;
+constexpr size_t kAlign = 256;
+
+size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+uint64_t fnv1a(uint64_t h, const void *data, size_t n) {
+    const unsigned char *p = static_cast<const unsigned char *>(data);
+    for (size_t i = 0; i < n; ++i) {
+        h ^= p[i];
+        h *= 1099511628211ull;
+    }
+    return h;
+}
+
+typedef CUresult (*PFN_writeValue32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+
+}  // namespace
+
+struct gr_ctx {
+    gr_world world{};
+    int32_t T = 0, G = 0, W = 0, nbits = 0, N = 1, rank = 0;
+    bool dry = false;
+    int buf_f16 = 1;
+    int64_t chunk_elems = kDefaultChunkElems;
+    int64_t one_shot_max_bytes = 0;
+    uint64_t hash = 0;
+
+    // host-side layouts
+    std::vector<int64_t> numel;
+    std::vector<int32_t> grad_f16, group_of, bit_of, tensor_of_bit, group_of_bit;
+    std::vector<int32_t> gbit_begin, gbit_end, gnchunks, gchunk_begin;
+    std::vector<int64_t> buf_off, gelems;
+    std::vector<Seg> segs;
+    std::vector<Chunk> chunks;
+    int64_t buf_elems = 0;
+    int32_t C = 0;
+
+    // device state
+    int dev = -1;
+    cudaStream_t s_coord = nullptr, s_data = nullptr, s_compute = nullptr;
+    cudaEvent_t ev_compute = nullptr, ev_data_done = nullptr;
+    cudaEvent_t ring_ev[GR_SLOT_RING] = {};
+    bool ring_pending[GR_SLOT_RING] = {};
+    char *symm = nullptr;
+    size_t symm_bytes = 0, off_slot = 0, off_pad = 0, off_buf = 0, pad_parity_u32 = 0;
+    size_t buf_parity_bytes = 0;
+    char *peer_symm[GR_MAX_RANKS] = {};
+    Seg *d_segs = nullptr;
+    Chunk *d_chunks = nullptr;
+    int32_t *d_tob = nullptr, *d_gob = nullptr, *d_gbb = nullptr, *d_gbe = nullptr, *d_gnch = nullptr,
+            *d_gcb = nullptr;
+    int64_t *d_gel = nullptr;
+    uint32_t *d_grel = nullptr, *d_ptr_epoch = nullptr;
+    uint64_t *d_ptr = nullptr;
+    int32_t *d_rel_ring = nullptr, *d_cum_ring = nullptr;
+    int32_t *d_counters = nullptr;  // [0] work, [1] done, [2] abort
+    // pinned host-mapped
+    uint32_t *h_bits = nullptr;   // sync marks, by bit
+    uint32_t *d_flags = nullptr;  // async marks (device memory), by bit
+    uint64_t *h_ptr = nullptr;
+    gr::HostResult *h_res = nullptr;
+    gr::HostError *h_err = nullptr;
+    uint32_t *d_hbits = nullptr;
+    uint64_t *d_hptr = nullptr;
+    gr::HostResult *d_res = nullptr;
+    gr::HostError *d_err = nullptr;
+    size_t res_bytes = 0;
+    PFN_writeValue32 write_value32 = nullptr;
+    int data_ctas[4] = {0, 0, 0, 0};
+
+    // step / cycle state
+    std::mutex mu;
+    std::vector<uint8_t> marked;
+    uint32_t epoch = 1;
+    int64_t cycle = 0, step = 0;
+    uint64_t seq = 0;
+    bool step_complete = false;
+    bool need_compute_fence = false;
+    int32_t abort_flag = 0, shutdown_flag = 0;
+    int sticky = 0;
+    int last_algo = GR_ALGO_NONE;
+    std::string err = "no error";
+
+    // stats / timing
+    gr_stats stats{};
+    bool timing = false;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pending_data_ev, pending_bv_ev, free_ev;
+};
+
+namespace {
+
+int fail(gr_ctx *c, int code, const char *fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    if (c) {
+        c->err = buf;
+        if (code == GR_ECUDA || code == GR_ETIMEOUT || code == GR_EABORT || code == GR_ESHUTDOWN)
+            c->sticky = code;
+    } else {
+        g_init_error = buf;
+    }
+    return code;
+}
+
+#define RC(expr)              \
+    do {                      \
+        int _rc = (expr);     \
+        if (_rc) return _rc;  \
+    } while (0)
+
+#define CK(c, expr)                                                                          \
+    do {                                                                                     \
+        cudaError_t _e = (expr);                                                             \
+        if (_e != cudaSuccess)                                                               \
+            return fail((c), GR_ECUDA, "%s failed: %s (%s:%d)", #expr, cudaGetErrorString(_e), \
+                        __FILE__, __LINE__);                                                 \
+    } while (0)
+
+// ---------------------------------------------------------------- layouts (host only)
+int build_layouts(gr_ctx *c, const gr_tensor *table, const int32_t *group_of) {
+    const int32_t T = c->T, G = c->G;
+    c->numel.resize(T);
+    c->grad_f16.resize(T);
+    c->group_of.assign(group_of, group_of + T);
+    std::vector<int32_t> members(G, 0);
+    for (int32_t t = 0; t < T; ++t) {
+        if (table[t].numel <= 0) return fail(nullptr, GR_EINVAL, "tensor %d: numel must be > 0", t);
+        if (table[t].grad_dtype != GR_F32 && table[t].grad_dtype != GR_F16)
+            return fail(nullptr, GR_EINVAL, "tensor %d: bad grad dtype", t);
+        if (group_of[t] < 0 || group_of[t] >= G)
+            return fail(nullptr, GR_EINVAL, "tensor %d: group id %d outside 0..%d", t, group_of[t], G - 1);
+        c->numel[t] = table[t].numel;
+        c->grad_f16[t] = table[t].grad_dtype == GR_F16;
+        members[group_of[t]]++;
+    }
+    for (int32_t g = 0; g < G; ++g)
+        if (!members[g]) return fail(nullptr, GR_EINVAL, "group %d is empty (ids must be dense)", g);
+
+    // response cache: group-major positions (reading R3)
+    std::vector<int32_t> order(T);
+    for (int32_t t = 0; t < T; ++t) order[t] = t;
+    std::stable_sort(order.begin(), order.end(),
+                     [&](int32_t a, int32_t b) { return group_of[a] < group_of[b]; });
+    c->nbits = GR_STATUS_BITS + T;
+    c->W = (c->nbits + 31) / 32;
+    c->bit_of.assign(T, 0);
+    c->tensor_of_bit.assign((size_t)c->W * 32, -1);
+    c->group_of_bit.assign((size_t)c->W * 32, -1);
+    c->gbit_begin.assign(G, INT32_MAX);
+    c->gbit_end.assign(G, -1);
+    for (int32_t pos = 0; pos < T; ++pos) {
+        const int32_t t = order[pos], b = GR_STATUS_BITS + pos, g = group_of[t];
+        c->bit_of[t] = b;
+        c->tensor_of_bit[b] = t;
+        c->group_of_bit[b] = g;
+        c->gbit_begin[g] = std::min(c->gbit_begin[g], b);
+        c->gbit_end[g] = std::max(c->gbit_end[g], b + 1);
+    }
+
+    // static fusion layout: same order, every tensor 8-element (16 B at fp16) aligned
+    c->buf_off.assign(T, 0);
+    c->gelems.assign(G, 0);
+    int64_t off = 0;
+    std::vector<int64_t> gbeg(G, -1), gend(G, 0);
+    for (int32_t pos = 0; pos < T; ++pos) {
+        const int32_t t = order[pos], g = group_of[t];
+        off = (off + 7) / 8 * 8;
+        if (gbeg[g] < 0) gbeg[g] = off;
+        c->buf_off[t] = off;
+        off += c->numel[t];
+        gend[g] = off;
+        c->gelems[g] += c->numel[t];
+    }
+    c->buf_elems = (off + 7) / 8 * 8;
+
+    // chunks: cut each group's range at chunk_elems, segments = tensor pieces
+    c->gchunk_begin.assign(G, 0);
+    c->gnchunks.assign(G, 0);
+    c->segs.clear();
+    c->chunks.clear();
+    int32_t pos = 0;
+    for (int32_t g = 0; g < G; ++g) {
+        c->gchunk_begin[g] = (int32_t)c->chunks.size();
+        const int32_t pos0 = pos;
+        while (pos < T && group_of[order[pos]] == g) ++pos;
+        for (int64_t cb = gbeg[g]; cb < gend[g]; cb += c->chunk_elems) {
+            const int64_t ce = std::min(gend[g], cb + c->chunk_elems);
+            Chunk ch;
+            ch.seg_begin = (int32_t)c->segs.size();
+            for (int32_t q = pos0; q < pos; ++q) {
+                const int32_t t = order[q];
+                const int64_t tb = c->buf_off[t], te = tb + c->numel[t];
+                const int64_t lo = std::max(tb, cb), hi = std::min(te, ce);
+                if (lo >= hi) continue;
+                Seg s;
+                s.tensor = t;
+                s.grad_f16 = c->grad_f16[t];
+                s.tensor_off = lo - tb;
+                s.buf_off = lo;
+                s.len = hi - lo;
+                c->segs.push_back(s);
+            }
+            ch.seg_end = (int32_t)c->segs.size();
+            c->chunks.push_back(ch);
+        }
+        c->gnchunks[g] = (int32_t)c->chunks.size() - c->gchunk_begin[g];
+    }
+    c->C = (int32_t)c->chunks.size();
+
+    // hash of everything that must agree across ranks (PAPER.md:108 global consistency)
+    uint64_t h = 1469598103934665603ull;
+    h = fnv1a(h, &c->N, sizeof c->N);
+    h = fnv1a(h, &c->T, sizeof c->T);
+    h = fnv1a(h, &c->G, sizeof c->G);
+    h = fnv1a(h, &c->buf_f16, sizeof c->buf_f16);
+    h = fnv1a(h, &c->chunk_elems, sizeof c->chunk_elems);
+    h = fnv1a(h, &c->one_shot_max_bytes, sizeof c->one_shot_max_bytes);
+    h = fnv1a(h, c->numel.data(), sizeof(int64_t) * T);
+    h = fnv1a(h, c->grad_f16.data(), sizeof(int32_t) * T);
+    h = fnv1a(h, c->group_of.data(), sizeof(int32_t) * T);
+    c->hash = h;
+    return GR_OK;
+}
+
+int allgather(gr_ctx *c, const void *send, void *recv, size_t bytes) {
+    if (c->N == 1) {
+        memcpy(recv, send, bytes);
+        return GR_OK;
+    }
+    if (!c->world.allgather) return fail(c, GR_EINVAL, "world.allgather is required when world_size > 1");
+    if (c->world.allgather(send, recv, bytes, c->world.user) != 0)
+        return fail(c, GR_EINVAL, "allgather callback failed");
+    return GR_OK;
+}
+
+template <typename T>
+int upload(gr_ctx *c, T **dst, const std::vector<T> &src) {
+    const size_t n = std::max<size_t>(1, src.size()) * sizeof(T);
+    CK(c, cudaMalloc((void **)dst, n));
+    if (!src.empty()) CK(c, cudaMemcpy(*dst, src.data(), src.size() * sizeof(T), cudaMemcpyHostToDevice));
+    return GR_OK;
+}
+
+int setup_device(gr_ctx *c) {
+    CK(c, cudaSetDevice(c->dev));
+    CK(c, cudaFree(nullptr));  // make sure the primary context exists
+    int lo = 0, hi = 0;
+    CK(c, cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    CK(c, cudaStreamCreateWithPriority(&c->s_coord, cudaStreamNonBlocking, hi));
+    CK(c, cudaStreamCreateWithPriority(&c->s_data, cudaStreamNonBlocking, hi));
+    c->s_compute = (cudaStream_t)c->world.compute_stream;
+    CK(c, cudaEventCreateWithFlags(&c->ev_compute, cudaEventDisableTiming));
+    CK(c, cudaEventCreateWithFlags(&c->ev_data_done, cudaEventDisableTiming));
+    for (int i = 0; i < GR_SLOT_RING; ++i) CK(c, cudaEventCreateWithFlags(&c->ring_ev[i], cudaEventDisableTiming));
+
+    // symmetric memory: [LL bitvector slots 2 x W u64][flag pad 2 x (C*N + C) u32][fusion buffer 2 x E]
+    const int esz = c->buf_f16 ? 2 : 4;
+    c->off_slot = 0;
+    c->off_pad = align_up(sizeof(uint64_t) * 2 * (size_t)c->W, kAlign);
+    c->pad_parity_u32 = (size_t)c->C * c->N + c->C;
+    c->off_buf = align_up(c->off_pad + sizeof(uint32_t) * 2 * c->pad_parity_u32, kAlign);
+    c->buf_parity_bytes = (c->N > 1) ? align_up((size_t)c->buf_elems * esz, kAlign) : 0;
+    c->symm_bytes = c->off_buf + 2 * c->buf_parity_bytes;
+    cudaError_t e = cudaMalloc((void **)&c->symm, c->symm_bytes);
+    if (e != cudaSuccess) return fail(c, GR_ENOMEM, "cudaMalloc(%zu) of symmetric memory: %s", c->symm_bytes, cudaGetErrorString(e));
+    CK(c, cudaMemset(c->symm, 0, c->off_buf));
+
+    RC(upload(c, &c->d_segs, c->segs));
+    RC(upload(c, &c->d_chunks, c->chunks));
+    RC(upload(c, &c->d_tob, c->tensor_of_bit));
+    RC(upload(c, &c->d_gob, c->group_of_bit));
+    RC(upload(c, &c->d_gbb, c->gbit_begin));
+    RC(upload(c, &c->d_gbe, c->gbit_end));
+    RC(upload(c, &c->d_gnch, c->gnchunks));
+    RC(upload(c, &c->d_gcb, c->gchunk_begin));
+    RC(upload(c, &c->d_gel, c->gelems));
+    CK(c, cudaMalloc((void **)&c->d_grel, sizeof(uint32_t) * c->G));
+    CK(c, cudaMemset(c->d_grel, 0, sizeof(uint32_t) * c->G));
+    CK(c, cudaMalloc((void **)&c->d_ptr_epoch, sizeof(uint32_t) * c->T));
+    CK(c, cudaMemset(c->d_ptr_epoch, 0, sizeof(uint32_t) * c->T));
+    CK(c, cudaMalloc((void **)&c->d_ptr, sizeof(uint64_t) * c->T));
+    CK(c, cudaMalloc((void **)&c->d_rel_ring, sizeof(int32_t) * GR_SLOT_RING * (size_t)c->G));
+    CK(c, cudaMalloc((void **)&c->d_cum_ring, sizeof(int32_t) * GR_SLOT_RING * (size_t)(c->G + 1)));
+    CK(c, cudaMalloc((void **)&c->d_counters, sizeof(int32_t) * 4));
+    CK(c, cudaMemset(c->d_counters, 0, sizeof(int32_t) * 4));
+
+    // pinned host-mapped: ready flags (by bit), pointer table, result block, error block
+    const unsigned hf = cudaHostAllocMapped | cudaHostAllocPortable;
+    CK(c, cudaHostAlloc((void **)&c->h_bits, sizeof(uint32_t) * (size_t)c->W, hf));
+    memset(c->h_bits, 0, sizeof(uint32_t) * (size_t)c->W);
+    CK(c, cudaMalloc((void **)&c->d_flags, sizeof(uint32_t) * (size_t)c->W * 32));
+    CK(c, cudaMemset(c->d_flags, 0, sizeof(uint32_t) * (size_t)c->W * 32));
+    CK(c, cudaHostAlloc((void **)&c->h_ptr, sizeof(uint64_t) * c->T, hf));
+    memset(c->h_ptr, 0, sizeof(uint64_t) * c->T);
+    c->res_bytes = sizeof(gr::HostResult) + sizeof(uint32_t) * c->W + sizeof(int32_t) * c->G;
+    CK(c, cudaHostAlloc((void **)&c->h_res, c->res_bytes, hf));
+    memset((void *)c->h_res, 0, c->res_bytes);
+    CK(c, cudaHostAlloc((void **)&c->h_err, sizeof(gr::HostError), hf));
+    memset((void *)c->h_err, 0, sizeof(gr::HostError));
+    CK(c, cudaHostGetDevicePointer((void **)&c->d_hbits, c->h_bits, 0));
+    CK(c, cudaHostGetDevicePointer((void **)&c->d_hptr, c->h_ptr, 0));
+    CK(c, cudaHostGetDevicePointer((void **)&c->d_res, (void *)c->h_res, 0));
+    CK(c, cudaHostGetDevicePointer((void **)&c->d_err, (void *)c->h_err, 0));
+
+    // stream memory operations for gr_mark_ready_async
+    void *fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+        c->write_value32 = (PFN_writeValue32)fn;
+
+    // data-kernel grid: every CTA co-resident (bounded by occupancy)
+    for (int algo = gr::ALGO_LOCAL; algo <= gr::ALGO_TWOSHOT; ++algo) {
+        int mx = 0;
+        int rc = gr::data_kernel_max_ctas(algo, c->buf_f16, &mx);
+        if (rc != 0) return fail(c, GR_ECUDA, "occupancy query failed: %s", cudaGetErrorString((cudaError_t)rc));
+        int want = c->world.comm_ctas > 0 ? c->world.comm_ctas : mx;
+        c->data_ctas[algo] = std::max(1, std::min(want, mx));
+    }
+    CK(c, cudaDeviceSynchronize());
+
+    // exchange IPC handles; this allgather is also the barrier after zeroing the pads
+    cudaIpcMemHandle_t mine;
+    memset(&mine, 0, sizeof mine);
+    if (c->N > 1) CK(c, cudaIpcGetMemHandle(&mine, c->symm));
+    std::vector<cudaIpcMemHandle_t> all(c->N);
+    int rc = allgather(c, &mine, all.data(), sizeof mine);
+    if (rc) return rc;
+    for (int r = 0; r < c->N; ++r) {
+        if (r == c->rank) {
+            c->peer_symm[r] = c->symm;
+            continue;
+        }
+        void *p = nullptr;
+        CK(c, cudaIpcOpenMemHandle(&p, all[r], cudaIpcMemLazyEnablePeerAccess));
+        c->peer_symm[r] = (char *)p;
+    }
+    return GR_OK;
+}
+
+void free_all(gr_ctx *c) {
+    if (c->dry || c->dev < 0) return;
+    cudaSetDevice(c->dev);
+    if (c->s_coord) cudaStreamSynchronize(c->s_coord);
+    if (c->s_data) cudaStreamSynchronize(c->s_data);
+    for (int r = 0; r < c->N; ++r)
+        if (r != c->rank && c->peer_symm[r]) cudaIpcCloseMemHandle(c->peer_symm[r]);
+    cudaFree(c->symm);
+    void *dptrs[] = {c->d_segs, c->d_chunks, c->d_tob, c->d_gob, c->d_gbb, c->d_gbe, c->d_gnch, c->d_gcb,
+                     c->d_gel, c->d_grel, c->d_ptr_epoch, c->d_ptr, c->d_rel_ring, c->d_cum_ring, c->d_counters,
+                     c->d_flags};
+    for (void *p : dptrs) cudaFree(p);
+    cudaFreeHost(c->h_bits);
+    cudaFreeHost(c->h_ptr);
+    cudaFreeHost((void *)c->h_res);
+    cudaFreeHost((void *)c->h_err);
+    for (int i = 0; i < GR_SLOT_RING; ++i)
+        if (c->ring_ev[i]) cudaEventDestroy(c->ring_ev[i]);
+    if (c->ev_compute) cudaEventDestroy(c->ev_compute);
+    if (c->ev_data_done) cudaEventDestroy(c->ev_data_done);
+    for (auto &v : {c->pending_data_ev, c->pending_bv_ev, c->free_ev})
+        for (auto &pr : v) {
+            cudaEventDestroy(pr.first);
+            cudaEventDestroy(pr.second);
+        }
+    if (c->s_coord) cudaStreamDestroy(c->s_coord);
+    if (c->s_data) cudaStreamDestroy(c->s_data);
+}
+
+std::pair<cudaEvent_t, cudaEvent_t> get_ev_pair(gr_ctx *c) {
+    if (!c->free_ev.empty()) {
+        auto pr = c->free_ev.back();
+        c->free_ev.pop_back();
+        return pr;
+    }
+    std::pair<cudaEvent_t, cudaEvent_t> pr;
+    cudaEventCreate(&pr.first);
+    cudaEventCreate(&pr.second);
+    return pr;
+}
+
+int collect_timing(gr_ctx *c) {
+    for (auto *v : {&c->pending_data_ev, &c->pending_bv_ev}) {
+        for (auto &pr : *v) {
+            float ms = 0.f;
+            CK(c, cudaEventSynchronize(pr.second));
+            CK(c, cudaEventElapsedTime(&ms, pr.first, pr.second));
+            if (v == &c->pending_data_ev) c->stats.data_kernel_ms += ms;
+            else c->stats.bitvector_kernel_ms += ms;
+            c->free_ev.push_back(pr);
+        }
+        v->clear();
+    }
+    return GR_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int gr_init(gr_ctx **out, const gr_world *world, const gr_tensor *table, int32_t T, const int32_t *group_of,
+            int32_t G) {
+    if (!out || !world || !table || !group_of) return fail(nullptr, GR_EINVAL, "null argument to gr_init");
+    *out = nullptr;
+    if (T <= 0 || G <= 0 || G > T) return fail(nullptr, GR_EINVAL, "need 0 < G <= T (T=%d, G=%d)", T, G);
+    if (world->world_size < 1 || world->world_size > GR_MAX_RANKS)
+        return fail(nullptr, GR_EINVAL, "world_size must be in 1..%d", GR_MAX_RANKS);
+    if (world->rank < 0 || world->rank >= world->world_size) return fail(nullptr, GR_EINVAL, "bad rank");
+    if (world->buffer_dtype != GR_F16 && world->buffer_dtype != GR_F32)
+        return fail(nullptr, GR_EINVAL, "bad buffer dtype");
+    if (world->chunk_elems < 0 || world->chunk_elems % 8)
+        return fail(nullptr, GR_EINVAL, "chunk_elems must be a non-negative multiple of 8");
+    gr_ctx *c = new (std::nothrow) gr_ctx();
+    if (!c) return fail(nullptr, GR_ENOMEM, "out of host memory");
+    c->world = *world;
+    c->T = T;
+    c->G = G;
+    c->N = world->world_size;
+    c->rank = world->rank;
+    c->buf_f16 = world->buffer_dtype == GR_F16;
+    c->chunk_elems = world->chunk_elems > 0 ? world->chunk_elems : kDefaultChunkElems;
+    // default one-shot threshold: at N=2 one-shot moves the same NVLink bytes as two-shot
+    // with one fewer synchronisation, so it is used at every size; above N=2 it is kept for
+    // latency-bound messages.
+    c->one_shot_max_bytes = world->one_shot_max_bytes >= 0 ? world->one_shot_max_bytes
+                                                           : (c->N == 2 ? INT64_MAX : (int64_t)1 << 20);
+    c->dry = world->device < 0;
+    if (c->world.timeout_ms <= 0) c->world.timeout_ms = kDefaultTimeoutMs;
+    int rc = build_layouts(c, table, group_of);
+    if (rc) {
+        delete c;
+        return rc;
+    }
+    c->marked.assign(T, 0);
+    // global consistency check: every rank must have built the same cache
+    std::vector<uint64_t> hashes(c->N);
+    rc = allgather(c, &c->hash, hashes.data(), sizeof(uint64_t));
+    if (rc) {
+        g_init_error = c->err;
+        delete c;
+        return rc;
+    }
+    for (int r = 0; r < c->N; ++r)
+        if (hashes[r] != c->hash) {
+            fail(nullptr, GR_EMISMATCH, "rank %d's tensor table / groups / config differ from rank %d's", r, c->rank);
+            delete c;
+            return GR_EMISMATCH;
+        }
+    if (!c->dry) {
+        c->dev = world->device;
+        rc = setup_device(c);
+        if (rc) {
+            g_init_error = c->err;
+            free_all(c);
+            delete c;
+            return rc;
+        }
+    }
+    *out = c;
+    return GR_OK;
+}
+
+static int mark_common(gr_ctx *c, int32_t rank, int32_t t, void *dev_ptr) {
+    if (!c) return GR_EINVAL;
+    if (c->dry) return fail(c, GR_ESTATE, "dry context (device < 0) cannot mark");
+    if (c->sticky) return fail(c, GR_ESTATE, "context is in a sticky error state (%d)", c->sticky);
+    if (rank != c->rank) return fail(c, GR_EINVAL, "rank %d != world.rank %d", rank, c->rank);
+    if (t < 0 || t >= c->T) return fail(c, GR_EINVAL, "tensor id %d out of range", t);
+    if (!dev_ptr) return fail(c, GR_EINVAL, "null dev_ptr for tensor %d", t);
+    if (c->step_complete) return fail(c, GR_ESTATE, "step complete: call gr_wait before marking again");
+    if (c->marked[t]) return fail(c, GR_ESTATE, "tensor %d already marked in this step", t);
+    c->marked[t] = 1;
+    c->h_ptr[t] = (uint64_t)(uintptr_t)dev_ptr;  // pointer first, then the flag
+    std::atomic_thread_fence(std::memory_order_release);
+    return GR_OK;
+}
+
+int gr_mark_ready(gr_ctx *c, int32_t rank, int32_t t, void *dev_ptr) {
+    if (!c) return GR_EINVAL;
+    std::lock_guard<std::mutex> lk(c->mu);
+    int rc = mark_common(c, rank, t, dev_ptr);
+    if (rc) return rc;
+    c->need_compute_fence = true;
+    const int32_t b = c->bit_of[t];
+    __atomic_fetch_or(&c->h_bits[b >> 5], 1u << (b & 31), __ATOMIC_RELEASE);
+    return GR_OK;
+}
+
+int gr_mark_ready_async(gr_ctx *c, int32_t rank, int32_t t, void *dev_ptr, void *stream) {
+    if (!c) return GR_EINVAL;
+    std::lock_guard<std::mutex> lk(c->mu);
+    if (!c->dry && !c->write_value32) return fail(c, GR_ECUDA, "cuStreamWriteValue32 unavailable");
+    int rc = mark_common(c, rank, t, dev_ptr);
+    if (rc) return rc;
+    CUresult r = c->write_value32((CUstream)stream, (CUdeviceptr)(c->d_flags + c->bit_of[t]), c->epoch, 0);
+    if (r != CUDA_SUCCESS) {
+        c->marked[t] = 0;
+        return fail(c, GR_ECUDA, "cuStreamWriteValue32 failed (%d)", (int)r);
+    }
+    return GR_OK;
+}
+
+int gr_set_status(gr_ctx *c, int32_t abort_flag, int32_t shutdown_flag) {
+    if (!c) return GR_EINVAL;
+    std::lock_guard<std::mutex> lk(c->mu);
+    c->abort_flag = abort_flag != 0;
+    c->shutdown_flag = shutdown_flag != 0;
+    return GR_OK;
+}
+
+int gr_step(gr_ctx *c, int32_t *released, gr_cycle_info *info, uint32_t *global_bits) {
+    if (!c || !released) return fail(c, GR_EINVAL, "null argument to gr_step");
+    if (c->dry) return fail(c, GR_ESTATE, "dry context (device < 0) cannot step");
+    if (c->sticky) return fail(c, GR_ESTATE, "context is in a sticky error state (%d): %s", c->sticky, c->err.c_str());
+    CK(c, cudaSetDevice(c->dev));
+    const int slot = (int)(c->cycle % GR_SLOT_RING);
+    if (c->ring_pending[slot]) {  // the data launch that read this slot must be done
+        CK(c, cudaEventSynchronize(c->ring_ev[slot]));
+        c->ring_pending[slot] = false;
+    }
+    uint32_t epoch;
+    int32_t abort_flag, shutdown_flag;
+    {
+        std::lock_guard<std::mutex> lk(c->mu);
+        if (c->step_complete) return fail(c, GR_ESTATE, "step complete: call gr_wait first");
+        if (c->need_compute_fence) {  // order the data stream after the marked gradients' producers
+            CK(c, cudaEventRecord(c->ev_compute, c->s_compute));
+            CK(c, cudaStreamWaitEvent(c->s_data, c->ev_compute, 0));
+            c->need_compute_fence = false;
+        }
+        epoch = c->epoch;
+        abort_flag = c->abort_flag;
+        shutdown_flag = c->shutdown_flag;
+    }
+
+    gr::BvParams p{};
+    p.host_bits = c->d_hbits;
+    p.dev_flags = c->d_flags;
+    p.host_ptr = c->d_hptr;
+    p.dev_ptr = c->d_ptr;
+    p.ptr_epoch = c->d_ptr_epoch;
+    p.tensor_of_bit = c->d_tob;
+    p.group_of_bit = c->d_gob;
+    p.group_bit_begin = c->d_gbb;
+    p.group_bit_end = c->d_gbe;
+    p.group_nchunks = c->d_gnch;
+    p.group_elems = c->d_gel;
+    p.group_rel_epoch = c->d_grel;
+    for (int r = 0; r < c->N; ++r) p.slot[r] = reinterpret_cast<uint64_t *>(c->peer_symm[r] + c->off_slot);
+    p.out_released = c->d_rel_ring + (size_t)slot * c->G;
+    p.out_cum = c->d_cum_ring + (size_t)slot * (c->G + 1);
+    p.result = c->d_res;
+    p.T = c->T;
+    p.G = c->G;
+    p.W = c->W;
+    p.nbits = c->nbits;
+    p.rank = c->rank;
+    p.N = c->N;
+    p.epoch = epoch;
+    p.tag = (uint32_t)(c->cycle + 1);
+    if (p.tag == 0) p.tag = 1;
+    p.parity = (int32_t)(c->cycle & 1);
+    p.abort_flag = abort_flag;
+    p.shutdown_flag = shutdown_flag;
+    p.timeout_ns = (uint64_t)c->world.timeout_ms * 1000000ull;
+    p.seq = ++c->seq;
+
+    std::pair<cudaEvent_t, cudaEvent_t> evb{};
+    if (c->timing) {
+        evb = get_ev_pair(c);
+        CK(c, cudaEventRecord(evb.first, c->s_coord));
+    }
+    int lrc = gr::launch_bitvector(p, c->s_coord);
+    if (lrc) return fail(c, GR_ECUDA, "bitvector launch: %s", cudaGetErrorString((cudaError_t)lrc));
+    if (c->timing) {
+        CK(c, cudaEventRecord(evb.second, c->s_coord));
+        c->pending_bv_ev.push_back(evb);
+    }
+    c->stats.bitvector_launches++;
+
+    // wait for the kernel's hand-off (pinned host memory), bounded
+    const auto t0 = std::chrono::steady_clock::now();
+    const auto limit = std::chrono::milliseconds(c->world.timeout_ms + 5000);
+    uint64_t spins = 0;
+    while (c->h_res->seq != p.seq) {
+        if ((++spins & 1023) == 0) {
+            cudaError_t q = cudaStreamQuery(c->s_coord);
+            if (q != cudaSuccess && q != cudaErrorNotReady)
+                return fail(c, GR_ECUDA, "bitvector kernel failed: %s", cudaGetErrorString(q));
+            if (std::chrono::steady_clock::now() - t0 > limit)
+                return fail(c, GR_ETIMEOUT, "bitvector kernel did not report within %d ms", c->world.timeout_ms + 5000);
+            if (spins > (1u << 20)) std::this_thread::yield();
+        }
+    }
+    std::atomic_thread_fence(std::memory_order_acquire);
+    const int status = c->h_res->status;
+    const uint32_t *hA = reinterpret_cast<const uint32_t *>(c->h_res + 1);
+    const int32_t *hrel = reinterpret_cast<const int32_t *>(hA + c->W);
+    if (global_bits) memcpy(global_bits, hA, sizeof(uint32_t) * c->W);
+    const int64_t this_cycle = c->cycle++;
+    c->stats.cycles++;
+    if (status == gr::ST_TIMEOUT) return fail(c, GR_ETIMEOUT, "cycle %lld: a peer did not publish its bitvector", (long long)this_cycle);
+    if (status == gr::ST_ABORT) return fail(c, GR_EABORT, "cycle %lld: a rank raised ABORT", (long long)this_cycle);
+    if (status == gr::ST_SHUTDOWN) return fail(c, GR_ESHUTDOWN, "cycle %lld: a rank raised SHUTDOWN", (long long)this_cycle);
+    const int n = c->h_res->n_released;
+    const int total_chunks = c->h_res->total_chunks;
+    const int64_t rel_elems = c->h_res->released_elems;
+    memcpy(released, hrel, sizeof(int32_t) * n);
+
+    if (n > 0) {
+        gr::DataParams d{};
+        d.segs = c->d_segs;
+        d.chunks = c->d_chunks;
+        d.group_chunk_begin = c->d_gcb;
+        d.released = p.out_released;
+        d.cum = p.out_cum;
+        d.dev_ptr = c->d_ptr;
+        const int par = (int)(epoch & 1);
+        for (int r = 0; r < c->N; ++r) {
+            char *base = c->peer_symm[r];
+            d.buf[r] = base + c->off_buf + (size_t)par * c->buf_parity_bytes;
+            uint32_t *pad = reinterpret_cast<uint32_t *>(base + c->off_pad) + (size_t)par * c->pad_parity_u32;
+            d.pack_flag[r] = pad;
+            d.rs_flag[r] = pad + (size_t)c->C * c->N;
+        }
+        d.work_counter = c->d_counters;
+        d.done_counter = c->d_counters + 1;
+        d.abort_dev = c->d_counters + 2;
+        d.err = c->d_err;
+        d.n_released = n;
+        d.total_chunks = total_chunks;
+        d.rank = c->rank;
+        d.N = c->N;
+        d.epoch = epoch;
+        d.inv_n = 1.0f / (float)c->N;
+        d.timeout_ns = (uint64_t)c->world.timeout_ms * 1000000ull;
+        const int64_t msg_bytes = rel_elems * (c->buf_f16 ? 2 : 4);
+        int algo = gr::ALGO_LOCAL;
+        if (c->N > 1) algo = msg_bytes <= c->one_shot_max_bytes ? gr::ALGO_ONESHOT : gr::ALGO_TWOSHOT;
+        const int nitems = total_chunks * (algo == gr::ALGO_LOCAL ? 1 : (algo == gr::ALGO_ONESHOT ? 2 : 3));
+        const int ctas = std::max(1, std::min(c->data_ctas[algo], nitems));
+        std::pair<cudaEvent_t, cudaEvent_t> evd{};
+        if (c->timing) {
+            evd = get_ev_pair(c);
+            CK(c, cudaEventRecord(evd.first, c->s_data));
+        }
+        lrc = gr::launch_data(d, algo, c->buf_f16, ctas, c->s_data);
+        if (lrc) return fail(c, GR_ECUDA, "data launch: %s", cudaGetErrorString((cudaError_t)lrc));
+        if (c->timing) {
+            CK(c, cudaEventRecord(evd.second, c->s_data));
+            c->pending_data_ev.push_back(evd);
+        }
+        CK(c, cudaEventRecord(c->ring_ev[slot], c->s_data));
+        c->ring_pending[slot] = true;
+        c->last_algo = algo;
+        c->stats.data_launches++;
+        c->stats.released_elems += rel_elems;
+    }
+    const int complete = c->h_res->step_complete;
+    {
+        std::lock_guard<std::mutex> lk(c->mu);
+        if (complete) c->step_complete = true;
+    }
+    if (info) {
+        info->n_released = n;
+        info->step_complete = complete;
+        info->cycle = this_cycle;
+        info->step = c->step;
+        info->released_elems = rel_elems;
+    }
+    return GR_OK;
+}
+
+int gr_wait(gr_ctx *c) {
+    if (!c) return GR_EINVAL;
+    if (c->dry) return fail(c, GR_ESTATE, "dry context (device < 0) cannot wait");
+    if (c->sticky == GR_ECUDA) return fail(c, GR_ESTATE, "context is in a sticky error state: %s", c->err.c_str());
+    CK(c, cudaSetDevice(c->dev));
+    CK(c, cudaStreamSynchronize(c->s_coord));
+    CK(c, cudaStreamSynchronize(c->s_data));
+    if (c->h_err->code) {
+        const int where = c->h_err->where;
+        return fail(c, GR_ETIMEOUT, "reduction timed out waiting for a peer (%s flag)", where == 1 ? "pack" : "reduce-scatter");
+    }
+    CK(c, cudaEventRecord(c->ev_data_done, c->s_data));
+    CK(c, cudaStreamWaitEvent(c->s_compute, c->ev_data_done, 0));
+    for (int i = 0; i < GR_SLOT_RING; ++i) c->ring_pending[i] = false;
+    if (c->timing) {
+        int rc = collect_timing(c);
+        if (rc) return rc;
+    }
+    std::lock_guard<std::mutex> lk(c->mu);
+    if (c->step_complete) {
+        c->step_complete = false;
+        c->epoch++;
+        if (c->epoch == 0) c->epoch = 1;
+        c->step++;
+        c->stats.steps++;
+        std::fill(c->marked.begin(), c->marked.end(), 0);
+        memset(c->h_bits, 0, sizeof(uint32_t) * (size_t)c->W);  // no bitvector kernel is in flight
+    }
+    return GR_OK;
+}
+
+int gr_finalize(gr_ctx *c) {
+    if (!c) return GR_OK;
+    free_all(c);
+    delete c;
+    return GR_OK;
+}
+
+const char *gr_last_error(gr_ctx *c) { return c ? c->err.c_str() : g_init_error.c_str(); }
+
+int gr_query(gr_ctx *c, int32_t kind, void *out, size_t bytes) {
+    if (!c || !out) return GR_EINVAL;
+    auto put = [&](const void *src, size_t n) -> int {
+        if (bytes < n) return fail(c, GR_EINVAL, "gr_query: need %zu bytes, got %zu", n, bytes);
+        memcpy(out, src, n);
+        return GR_OK;
+    };
+    switch (kind) {
+        case GR_Q_WORDS: return put(&c->W, sizeof(int32_t));
+        case GR_Q_BIT_OF: return put(c->bit_of.data(), sizeof(int32_t) * c->T);
+        case GR_Q_BUF_OFFSET: return put(c->buf_off.data(), sizeof(int64_t) * c->T);
+        case GR_Q_NCHUNKS: return put(&c->C, sizeof(int32_t));
+        case GR_Q_STATS: return put(&c->stats, sizeof(gr_stats));
+        case GR_Q_LAST_ALGO: return put(&c->last_algo, sizeof(int32_t));
+        default: return fail(c, GR_EINVAL, "unknown query %d", kind);
+    }
+}
+
+int gr_set_timing(gr_ctx *c, int32_t on) {
+    if (!c) return GR_EINVAL;
+    c->timing = on != 0;
+    return GR_OK;
+}
+
+int gr_reset_stats(gr_ctx *c) {
+    if (!c) return GR_EINVAL;
+    c->stats = gr_stats{};
+    return GR_OK;
+}
+
+int gr_bench_spin(int64_t ns, int32_t ctas, void *stream) {
+    if (ns < 0 || ctas <= 0) return GR_EINVAL;
+    return gr::launch_spin(ns, ctas, stream) ? GR_ECUDA : GR_OK;
+}
+
+}  // extern "C"

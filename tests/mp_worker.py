@@ -1,0 +1,111 @@
+"""torchrun worker for the multi-GPU parity tests (one process per GPU).
+
+  torchrun --nproc-per-node N --master-addr 127.0.0.1 tests/mp_worker.py --suite cfg1 --seeds 0:20
+
+Every rank replays the same seeded schedules through the C ABI, checks its own
+schedule and values against the oracle (tests/parity_lib.py) and the ranks
+compare output hashes (bitwise-identical replicas). Exit code 0 = all passed.
+"""
+from __future__ import annotations
+
+import argparse
+import os
+import sys
+import traceback
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--suite", default="cfg1")
+    ap.add_argument("--seeds", default="0:10")
+    ap.add_argument("--buffers", default="f16,f32")
+    ap.add_argument("--one-shot-max-bytes", type=int, default=-1)
+    ap.add_argument("--chunk-elems", type=int, default=0)
+    args = ap.parse_args()
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_1909_11150_b200 import GR_F16, GR_F32, Context, make_allgather
+    from tests.parity_lib import run_case_on_rank
+    from workloads import cfg1_case, fcn220m
+    from workloads.schedules import Case, random_mark_schedule, random_partition, reverse_layer_schedule
+
+    rank = int(os.environ["RANK"])
+    N = int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    dist.init_process_group("gloo")
+    ag = make_allgather(None)
+    dev = torch.device("cuda", local)
+    s0, s1 = (int(x) for x in args.seeds.split(":"))
+    failures = 0
+    ncase = 0
+
+    def run(case, seed, buf, grad_f16=None, kind="uniform", chunk=0, osm=None, max_cycles=None):
+        nonlocal failures, ncase
+        ncase += 1
+        ctx = Context(rank=rank, world_size=N, device=local, numel=case.numel, group_of=case.group_of,
+                      grad_f16=grad_f16, buffer_dtype=GR_F16 if buf == "f16" else GR_F32,
+                      one_shot_max_bytes=args.one_shot_max_bytes if osm is None else osm,
+                      chunk_elems=chunk or args.chunk_elems, timeout_ms=20000, allgather=ag)
+        ok = True
+        try:
+            _log, h = run_case_on_rank(ctx, case, rank, seed, dev, buf == "f16", grad_f16, kind,
+                                       max_cycles=max_cycles)
+        except AssertionError as e:
+            ok = False
+            h = "FAIL"
+            print(f"[rank {rank}] seed {seed} buf {buf}: {e}", flush=True)
+        hs = [None] * N
+        dist.all_gather_object(hs, h)
+        if ok and len(set(hs)) != 1:
+            ok = False
+            print(f"[rank {rank}] seed {seed} buf {buf}: outputs differ across ranks {hs}", flush=True)
+        failures += (not ok)
+        ctx.gr_finalize()
+
+    try:
+        for buf in args.buffers.split(","):
+            if args.suite == "cfg1":
+                for seed in range(s0, s1):
+                    case = cfg1_case(seed, N=N)
+                    run(case, seed, buf)
+            elif args.suite == "edge":
+                # ragged sizes, many chunks, both algorithms, fp16 grads, integer payloads
+                for seed in range(s0, s1):
+                    rng = np.random.default_rng(seed)
+                    T = int(rng.integers(1, 24))
+                    G = int(rng.integers(1, T + 1))
+                    numel = rng.integers(1, 200000, size=T).astype(np.int64)
+                    numel[rng.integers(0, T)] = int(rng.integers(1, 9))
+                    case = Case(N, numel, random_partition(T, G, rng), random_mark_schedule(N, T, seed, 3), seed)
+                    gf = (rng.random(T) < 0.3).tolist()
+                    for osm in (0, 1 << 62):  # force two-shot, force one-shot
+                        run(case, seed, buf, grad_f16=gf, chunk=int(rng.choice([1024, 4096, 32768])), osm=osm)
+                    run(case, seed, buf, kind="int", osm=0)
+            elif args.suite == "fcn":
+                f = fcn220m()
+                mark = reverse_layer_schedule(len(f.layers), N, f.release_order, layers_per_cycle=1,
+                                              jitter_seed=s0, max_shift=2)
+                case = Case(N, f.numel, f.group_of, mark, s0)
+                run(case, s0, buf)
+            else:
+                raise SystemExit(f"unknown suite {args.suite}")
+    except Exception:
+        traceback.print_exc()
+        failures += 1
+    tot = [None] * N
+    dist.all_gather_object(tot, failures)
+    if rank == 0:
+        print(f"mp_worker suite={args.suite} N={N} cases={ncase} failures={sum(tot)}", flush=True)
+    dist.destroy_process_group()
+    sys.exit(1 if sum(tot) else 0)
+
+
+if __name__ == "__main__":
+    main()

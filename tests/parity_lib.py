@@ -1,0 +1,101 @@
+"""GPU-vs-oracle parity checks shared by the -m gpu tests, the torchrun worker
+(tests/mp_worker.py) and __graft_entry__.smoke().
+
+The bar:
+* schedule: per cycle, the intersected bitvector A_c (status bits included)
+  and the released group list are BIT-EXACT against oracle.simulate_step;
+* values: every reduced gradient element is bit-exact against
+  oracle.emulate (fp32 rank-order sum, x fl32(1/N), buffer/grad rounding —
+  readings R7-R9), AND within the north-star tolerance of the fp64 reference
+  oracle.reduce_f64: |out-ref| <= 1e-6*max(|ref|, mean_r|g_r|) for fp32
+  buffers (reading R10), |out-ref| <= 2^-10*N*max|g| for fp16 (reading R11);
+* cross-rank: gradients identical bit for bit on every rank (checked by the
+  caller through a hash allgather).
+"""
+from __future__ import annotations
+
+import hashlib
+
+import numpy as np
+
+import oracle
+from harness.replay import make_grads, replay_step
+from workloads.values import tensor_scales, values_np
+
+
+def sample_indices(n: int, seed: int, full_below: int = 1 << 20, k: int = 1 << 16):
+    """All indices of small tensors; for large ones the head, the tail and k random ones."""
+    if n <= full_below:
+        return np.arange(n)
+    rng = np.random.default_rng(seed)
+    return np.unique(np.concatenate([np.arange(4096), np.arange(n - 4096, n), rng.integers(0, n, k)]))
+
+
+def host_inputs(numel, N, seed, t, grad_f16_t: bool, kind: str = "uniform", idx=None):
+    s = tensor_scales(seed, len(numel))
+    if idx is None:
+        idx = np.arange(int(numel[t]))
+    gs = []
+    for r in range(N):
+        v = values_np(seed, r, t, idx, float(s[t]), kind)
+        if grad_f16_t:
+            v = v.astype(np.float16).astype(np.float32)
+        gs.append(v)
+    return gs
+
+
+def check_schedule(log, ref, where=""):
+    assert log.n_cycles == ref.n_cycles, f"{where}: cycles gpu={log.n_cycles} oracle={ref.n_cycles}"
+    for c in range(ref.n_cycles):
+        assert [int(x) for x in log.A[c]] == [int(x) for x in ref.A[c]], \
+            f"{where}: cycle {c} A gpu={log.A[c]} oracle={list(ref.A[c])}"
+        assert log.released[c] == ref.released[c], \
+            f"{where}: cycle {c} released gpu={log.released[c]} oracle={ref.released[c]}"
+
+
+def check_values(out_np, gs, N, buffer_f16: bool, grad_f16_t: bool, where=""):
+    emu = oracle.emulate(gs, buffer_f16, grad_f16_t)
+    ref = oracle.reduce_f64(gs)
+    out = out_np.astype(np.float32)
+    bad = np.nonzero(out.view(np.uint32) != emu.view(np.uint32))[0]
+    assert bad.size == 0, (f"{where}: {bad.size} elements differ from the oracle emulation, first "
+                           f"i={bad[0]} gpu={out[bad[0]]!r} emu={emu[bad[0]]!r}")
+    o64 = out.astype(np.float64)
+    stack = np.stack(gs).astype(np.float64)
+    if buffer_f16:
+        tol = 2.0 ** -10 * N * float(np.max(np.abs(stack)))
+        assert np.all(np.abs(o64 - ref) <= tol), f"{where}: fp16 tolerance violated"
+    else:
+        bound = 1e-6 * np.maximum(np.abs(ref), np.mean(np.abs(stack), axis=0))
+        if grad_f16_t:  # fp16 gradient storage adds one output rounding (half an fp16 ulp)
+            bound = bound + np.abs(ref) * 2.0 ** -11 + 2.0 ** -25
+        assert np.all(np.abs(o64 - ref) <= bound), f"{where}: fp32 tolerance violated"
+
+
+def run_case_on_rank(ctx, case, r, seed, device, buffer_f16: bool, grad_f16=None, kind="uniform",
+                     max_cycles=None, async_stream=None):
+    """Replay `case` on rank r through the C ABI and check it against the oracle.
+    Returns (log, sha256 of all output gradients) for the cross-rank comparison."""
+    import torch
+
+    T = case.T
+    if max_cycles is None:
+        max_cycles = int(np.max(case.mark_cycle)) + 2
+    grads = make_grads(case.numel, r, seed, device, grad_f16, kind)
+    torch.cuda.synchronize(device)
+    log = replay_step(ctx, case.mark_cycle[r], [g.data_ptr() for g in grads], max_cycles,
+                      async_stream=async_stream)
+    ref = oracle.simulate_step(case.N, case.group_of, case.mark_cycle, max_cycles=max_cycles)
+    check_schedule(log, ref, where=f"rank {r} seed {seed}")
+    released_groups = {g for rel in ref.released for g in rel}
+    h = hashlib.sha256()
+    for t in range(T):
+        f16 = bool(grad_f16 is not None and grad_f16[t])
+        out = grads[t].float().cpu().numpy()
+        h.update(out.tobytes())
+        if int(case.group_of[t]) not in released_groups:
+            continue
+        idx = sample_indices(out.size, seed * 7919 + t)
+        gs = host_inputs(case.numel, case.N, seed, t, f16, kind, idx)
+        check_values(out[idx], gs, case.N, buffer_f16, f16, where=f"rank {r} seed {seed} tensor {t}")
+    return log, h.hexdigest()

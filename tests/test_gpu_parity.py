@@ -1,0 +1,197 @@
+"""GPU parity: the CUDA path (through the C ABI) against the oracle.
+
+N=1 cases run in-process on cuda:0. N>1 cases launch tests/mp_worker.py
+under torchrun (one process per GPU) and are skipped when the box has fewer
+GPUs. Both paths check schedule bit-exactness, value bit-exactness against the
+oracle's emulation, the north-star tolerances and cross-rank identity
+(tests/parity_lib.py).
+"""
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+from tests.conftest import ROOT, gpu_count
+from workloads import cfg1_case, fcn220m
+from workloads.schedules import Case, random_mark_schedule, random_partition, reverse_layer_schedule
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def gpu():
+    if gpu_count() < 1:
+        pytest.skip("no GPU")
+    import torch
+    torch.cuda.set_device(0)
+    return torch.device("cuda", 0)
+
+
+def _ctx(case, buf16, **kw):
+    from paper_1909_11150_b200 import GR_F16, GR_F32, Context
+    return Context(rank=0, world_size=1, device=0, numel=case.numel, group_of=case.group_of,
+                   buffer_dtype=GR_F16 if buf16 else GR_F32, timeout_ms=5000, **kw)
+
+
+def _n1(case):
+    return Case(1, case.numel, case.group_of, case.mark_cycle[:1].copy(), case.seed)
+
+
+@pytest.mark.parametrize("buf16", [True, False])
+def test_cfg1_n1_many_seeds(gpu, buf16):
+    from tests.parity_lib import run_case_on_rank
+    for seed in range(40):
+        case = _n1(cfg1_case(seed))
+        ctx = _ctx(case, buf16)
+        run_case_on_rank(ctx, case, 0, seed, gpu, buf16)
+        ctx.gr_finalize()
+
+
+def test_same_context_many_steps(gpu):
+    """Epoch handling: the same context across 6 steps with different schedules."""
+    from tests.parity_lib import run_case_on_rank
+    base = cfg1_case(3)
+    ctx = _ctx(_n1(base), True)
+    for step in range(6):
+        mark = random_mark_schedule(1, base.T, 100 + step)
+        case = Case(1, base.numel, base.group_of, mark, 100 + step)
+        run_case_on_rank(ctx, case, 0, 100 + step, gpu, True)
+    assert ctx.stats().steps == 6
+    ctx.gr_finalize()
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_edge_shapes_n1(gpu, seed):
+    """Ragged sizes (1..7 elements, non-multiples of 8), tensors spanning many
+    chunks, tiny chunks, fp16 gradients, integer payloads, G=1 and singletons."""
+    from tests.parity_lib import run_case_on_rank
+    rng = np.random.default_rng(seed)
+    T = int(rng.integers(1, 30))
+    numel = rng.integers(1, 300000, size=T).astype(np.int64)
+    numel[: min(T, 3)] = rng.integers(1, 8, size=min(T, 3))
+    G = [1, T, int(rng.integers(1, T + 1))][seed % 3]
+    case = Case(1, numel, random_partition(T, G, rng), random_mark_schedule(1, T, seed, 3), seed)
+    gf = (rng.random(T) < 0.4).tolist()
+    for buf16 in (True, False):
+        for chunk in (8, 1024, 32768):
+            ctx = _ctx(case, buf16, chunk_elems=chunk, grad_f16=gf)
+            run_case_on_rank(ctx, case, 0, seed, gpu, buf16, grad_f16=gf)
+            ctx.gr_finalize()
+        ctx = _ctx(case, buf16)
+        run_case_on_rank(ctx, case, 0, seed, gpu, buf16, kind="int")
+        ctx.gr_finalize()
+
+
+def test_unaligned_pointer_scalar_path(gpu):
+    """A gradient view starting 1 element into its storage takes the scalar path."""
+    import torch
+    from paper_1909_11150_b200 import GR_F16, Context
+    from tests.parity_lib import check_values
+    n = 10001
+    base = torch.empty(n + 1, device=gpu)
+    base.uniform_(-1, 1)
+    g = base[1:]
+    src = g.cpu().numpy().copy()
+    ctx = Context(rank=0, world_size=1, device=0, numel=[n], group_of=[0], buffer_dtype=GR_F16)
+    ctx.gr_mark_ready(0, g.data_ptr())
+    rel, complete, A, _ = ctx.gr_step()
+    ctx.gr_wait()
+    assert rel == [0] and complete and A == [0b111]
+    check_values(g.cpu().numpy(), [src], 1, True, False)
+    ctx.gr_finalize()
+
+
+def test_never_marked_and_errors(gpu):
+    import torch
+    from paper_1909_11150_b200 import GR_F16, Context, GrError
+    from paper_1909_11150_b200.binding import GR_EINVAL, GR_ESTATE, GR_EABORT
+    x = torch.zeros(64, device=gpu)
+    ctx = Context(rank=0, world_size=1, device=0, numel=[64, 64], group_of=[0, 1], buffer_dtype=GR_F16)
+    ctx.gr_mark_ready(0, x.data_ptr())
+    with pytest.raises(GrError) as e:
+        ctx.gr_mark_ready(0, x.data_ptr())          # duplicate mark
+    assert e.value.code == GR_ESTATE
+    with pytest.raises(GrError) as e:
+        ctx.gr_mark_ready(5, x.data_ptr())          # bad id
+    assert e.value.code == GR_EINVAL
+    with pytest.raises(GrError) as e:
+        ctx.gr_mark_ready(1, x.data_ptr(), rank=1)  # wrong rank
+    assert e.value.code == GR_EINVAL
+    for _ in range(3):                              # tensor 1 never marked: group 1 stays pending
+        rel, complete, A, _ = ctx.gr_step()
+        assert not complete
+    ctx.gr_set_status(abort=True)
+    with pytest.raises(GrError) as e:
+        ctx.gr_step()
+    assert e.value.code == GR_EABORT
+    with pytest.raises(GrError) as e:               # sticky
+        ctx.gr_step()
+    assert e.value.code == GR_ESTATE
+    ctx.gr_finalize()
+
+
+def test_async_marks_follow_stream(gpu):
+    """gr_mark_ready_async: the flag lands only after the stream's prior work."""
+    import torch
+    from paper_1909_11150_b200 import GR_F32, Context, gr_bench_spin
+    s = torch.cuda.Stream(device=gpu)
+    x = torch.ones(1024, device=gpu)
+    ctx = Context(rank=0, world_size=1, device=0, numel=[1024], group_of=[0], buffer_dtype=GR_F32)
+    with torch.cuda.stream(s):
+        gr_bench_spin(200_000_000, 4, s.cuda_stream)          # 200 ms of "backward"
+        x.mul_(3.0)
+    ctx.gr_mark_ready_async(0, x.data_ptr(), s.cuda_stream)
+    rel, complete, _, _ = ctx.gr_step()                     # the spin is still running
+    assert rel == [] and not complete
+    s.synchronize()
+    rel, complete, _, _ = ctx.gr_step()
+    assert rel == [0] and complete
+    ctx.gr_wait()
+    assert torch.equal(x, torch.full_like(x, 3.0))
+    ctx.gr_finalize()
+
+
+def test_fcn220m_n1_full_size(gpu):
+    """The bench workload at full size (225,115,137 elements, 68 tensors,
+    10 groups), reverse-layer schedule; values checked on sampled elements."""
+    from tests.parity_lib import run_case_on_rank
+    f = fcn220m()
+    mark = reverse_layer_schedule(len(f.layers), 1, f.release_order, layers_per_cycle=3)
+    case = Case(1, f.numel, f.group_of, mark, 21)
+    for buf16 in (True, False):
+        ctx = _ctx(case, buf16)
+        run_case_on_rank(ctx, case, 0, 21, gpu, buf16)
+        ctx.gr_finalize()
+
+
+def _torchrun(n, *args, timeout=900):
+    env = dict(os.environ, PYTHONPATH=ROOT)
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(29500 + n), os.path.join(ROOT, "tests", "mp_worker.py"),
+           *args]
+    r = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=timeout, cwd=ROOT)
+    print(r.stdout[-4000:], r.stderr[-4000:])
+    return r.returncode
+
+
+@pytest.mark.parametrize("n", [2, 4, 8])
+def test_multi_gpu_cfg1(n):
+    if gpu_count() < n:
+        pytest.skip(f"needs {n} GPUs")
+    assert _torchrun(n, "--suite", "cfg1", "--seeds", "0:30") == 0
+
+
+@pytest.mark.parametrize("n", [2, 4, 8])
+def test_multi_gpu_edge(n):
+    if gpu_count() < n:
+        pytest.skip(f"needs {n} GPUs")
+    assert _torchrun(n, "--suite", "edge", "--seeds", "0:4") == 0
+
+
+@pytest.mark.parametrize("n", [2, 4, 8])
+def test_multi_gpu_fcn220m(n):
+    if gpu_count() < n:
+        pytest.skip(f"needs {n} GPUs")
+    assert _torchrun(n, "--suite", "fcn", "--seeds", "5:6") == 0
