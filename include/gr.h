@@ -185,9 +185,17 @@ typedef struct {
     int64_t released_elems;     /* gradient elements reduced */
     double data_kernel_ms;      /* summed device time of data launches (only with timing on) */
     double bitvector_kernel_ms; /* summed device time of bitvector launches (only with timing on) */
+    double host_step_us;        /* summed host wall time inside gr_step */
+    double host_wait_us;        /* part of it spent waiting for the bitvector kernel's hand-off */
+    double bitvector_device_us; /* summed %globaltimer span of the bitvector kernels (start->hand-off) */
 } gr_stats;
 
 int gr_query(gr_ctx *ctx, int32_t kind, void *out, size_t bytes);
+
+/* Tracing: with the environment variable GR_TRACE=<prefix> set at gr_init, every
+ * cycle's bitvector-kernel phase stamps and every data launch's per-item
+ * (grab, ready, done, CTA/SM) %globaltimer stamps are appended at gr_wait to
+ * <prefix>.rank<r>.jsonl (the analogue of the paper's Horovod Timeline, Fig.2). */
 
 /* gr_set_timing — LOCAL. 1 = bracket every kernel launch with CUDA events on
  * its own stream and accumulate device time into gr_stats (default 0).

@@ -44,7 +44,9 @@ class GrCycleInfo(ctypes.Structure):
 class GrStats(ctypes.Structure):
     _fields_ = [("cycles", ctypes.c_int64), ("steps", ctypes.c_int64), ("bitvector_launches", ctypes.c_int64),
                 ("data_launches", ctypes.c_int64), ("released_elems", ctypes.c_int64),
-                ("data_kernel_ms", ctypes.c_double), ("bitvector_kernel_ms", ctypes.c_double)]
+                ("data_kernel_ms", ctypes.c_double), ("bitvector_kernel_ms", ctypes.c_double),
+                ("host_step_us", ctypes.c_double), ("host_wait_us", ctypes.c_double),
+                ("bitvector_device_us", ctypes.c_double)]
 
 
 class GrError(RuntimeError):
@@ -102,7 +104,7 @@ def make_allgather(pg=None, device=None):
             backend = dist.get_backend(pg)
             dev = torch.device("cuda", device) if (backend == "nccl" and device is not None) else \
                 (torch.device("cuda", torch.cuda.current_device()) if backend == "nccl" else torch.device("cpu"))
-            src = torch.frombuffer(ctypes.string_at(send, nbytes), dtype=torch.uint8).to(dev)
+            src = torch.frombuffer(bytearray(ctypes.string_at(send, nbytes)), dtype=torch.uint8).to(dev)
             out = torch.empty(ws * nbytes, dtype=torch.uint8, device=dev)
             dist.all_gather_into_tensor(out, src, group=pg)
             data = out.cpu().numpy().tobytes()

@@ -6,6 +6,7 @@
 #define GR_MAX_RANKS 8
 #define GR_STATUS_BITS 2
 #define GR_SLOT_RING 64            // released-list slots in flight (cycle % ring)
+#define GR_BV_INLINE_WORDS 64      // host mark bits passed as kernel parameters up to this W
 
 namespace gr {
 
@@ -32,6 +33,7 @@ struct HostResult {
     int32_t step_complete;
     int32_t total_chunks;
     int64_t released_elems;
+    uint64_t t_start, t_populated, t_anded, t_end;  // %globaltimer (ns) phase stamps
 };
 
 struct HostError {
@@ -42,11 +44,9 @@ struct HostError {
 enum { ST_OK = 0, ST_ABORT = 1, ST_SHUTDOWN = 2, ST_TIMEOUT = 3 };
 
 struct BvParams {
-    const uint32_t *host_bits;       // host-mapped [W]: bits set by gr_mark_ready (cleared per step)
+    const uint32_t *host_bits;       // host-mapped [W]: bits set by gr_mark_ready (cleared per step);
+                                     // unused when W <= GR_BV_INLINE_WORDS (copied into inline_bits)
     const uint32_t *dev_flags;       // device [W*32]: step epoch written by gr_mark_ready_async
-    const uint64_t *host_ptr;        // host-mapped [T]
-    uint64_t *dev_ptr;               // device [T]
-    uint32_t *ptr_epoch;             // device [T]: epoch whose pointer dev_ptr holds
     const int32_t *tensor_of_bit;    // device [nbits]
     const int32_t *group_of_bit;     // device [nbits]
     const int32_t *group_bit_begin;  // device [G]
@@ -65,6 +65,8 @@ struct BvParams {
     int32_t abort_flag, shutdown_flag;
     uint64_t timeout_ns;
     uint64_t seq;
+    int32_t use_inline;
+    uint32_t inline_bits[GR_BV_INLINE_WORDS];  // snapshot of host_bits passed with the launch
 };
 
 enum Algo { ALGO_LOCAL = 1, ALGO_ONESHOT = 2, ALGO_TWOSHOT = 3 };
@@ -83,6 +85,7 @@ struct DataParams {
     int32_t *done_counter;
     volatile int32_t *abort_dev;       // device flag: bail out (set on timeout)
     HostError *err;                    // host-mapped
+    uint64_t *trace;                   // optional [items][4]: grab, ready, done, cta|smid<<32
     int32_t n_released, total_chunks;
     int32_t rank, N;
     uint32_t epoch;

@@ -65,8 +65,14 @@ __device__ __forceinline__ void fence_acq_rel_sys() { asm volatile("fence.acq_re
 // ---------------------------------------------------------------------------------------
 // K1: bitvector populate + AND + release
 // ---------------------------------------------------------------------------------------
-constexpr int BV_THREADS = 512;
-constexpr int BV_BATCH = 8;
+#ifndef GR_BV_THREADS
+#define GR_BV_THREADS 512
+#endif
+#ifndef GR_BV_BATCH
+#define GR_BV_BATCH 8
+#endif
+constexpr int BV_THREADS = GR_BV_THREADS;
+constexpr int BV_BATCH = GR_BV_BATCH;
 
 __global__ void __launch_bounds__(BV_THREADS, 1) bitvector_kernel(BvParams p) {
     extern __shared__ uint32_t smem[];
@@ -79,6 +85,7 @@ __global__ void __launch_bounds__(BV_THREADS, 1) bitvector_kernel(BvParams p) {
     __shared__ int s_all[32];
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
+    const uint64_t t_start = globaltimer();
     if (tid == 0) { s_timeout = 0; s_elems = 0ull; }
 
     // ---- step 1: populate from pending requests, publish ----
@@ -94,7 +101,7 @@ __global__ void __launch_bounds__(BV_THREADS, 1) bitvector_kernel(BvParams p) {
             const int b = w * 32 + lane;
             const bool valid = w < p.W && b >= GR_STATUS_BITS && b < p.nbits;
             f[k] = valid ? ld_relaxed_sys32(p.dev_flags + b) : 0u;
-            hb[k] = (w < p.W) ? ld_relaxed_sys32(p.host_bits + w) : 0u;
+            hb[k] = (w < p.W) ? (p.use_inline ? p.inline_bits[w] : ld_relaxed_sys32(p.host_bits + w)) : 0u;
             gob[k] = valid ? p.group_of_bit[b] : -1;
         }
 #pragma unroll
@@ -104,15 +111,7 @@ __global__ void __launch_bounds__(BV_THREADS, 1) bitvector_kernel(BvParams p) {
             const int b = w * 32 + lane;
             bool pend = false;
             if (gob[k] >= 0 && (f[k] == p.epoch || ((hb[k] >> lane) & 1u))) {
-                if (p.group_rel_epoch[gob[k]] != p.epoch) {
-                    pend = true;
-                    const int t = p.tensor_of_bit[b];
-                    if (p.ptr_epoch[t] != p.epoch) {           // first sighting this step: fetch ptr
-                        fence_acq_rel_sys();                   // mark read -> pointer read
-                        p.dev_ptr[t] = ld_relaxed_sys64(p.host_ptr + t);
-                        p.ptr_epoch[t] = p.epoch;
-                    }
-                }
+                pend = p.group_rel_epoch[gob[k]] != p.epoch;
             } else if (b == 0) {
                 pend = !p.abort_flag;     // complement-coded status bits (R1)
             } else if (b == 1) {
@@ -126,6 +125,7 @@ __global__ void __launch_bounds__(BV_THREADS, 1) bitvector_kernel(BvParams p) {
         }
     }
     __syncthreads();
+    const uint64_t t_populated = globaltimer();
 
     // ---- step 2: A = AND_r L_r. Lane group of GS lanes per word, lane rr
     // holds rank rr's copy (own from smem, peers via NVLink LL loads). ----
@@ -171,6 +171,7 @@ __global__ void __launch_bounds__(BV_THREADS, 1) bitvector_kernel(BvParams p) {
         }
     }
     __syncthreads();
+    const uint64_t t_anded = globaltimer();
 
     // ---- status bits (R1, R13) ----
     int status = ST_OK;
@@ -259,8 +260,11 @@ __global__ void __launch_bounds__(BV_THREADS, 1) bitvector_kernel(BvParams p) {
         p.result->step_complete = (status == ST_OK) ? complete : 0;
         p.result->total_chunks = run_ch;
         p.result->released_elems = (int64_t)s_elems;
-        fence_sys();
-        p.result->seq = p.seq;
+        p.result->t_start = t_start;
+        p.result->t_populated = t_populated;
+        p.result->t_anded = t_anded;
+        p.result->t_end = globaltimer();
+        asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(&p.result->seq), "l"(p.seq) : "memory");
     }
 }
 
@@ -572,53 +576,67 @@ __global__ void __launch_bounds__(DATA_THREADS) data_kernel(DataParams p) {
         const int item = s_item;
         __syncthreads();
         if (item >= nphase * total) break;
+        uint64_t t_grab = 0, t_ready = 0;
+        if (p.trace && tid == 0) t_grab = globaltimer();
         const int phase = item / total;
         const int c = chunk_of_item(p, item - phase * total);
         const int owner = c % p.N;
         if (ALGO == ALGO_LOCAL) {
             process_chunk<BT, OP_LOCAL>(p, c, 0);
-        } else if (phase == 0) {  // pack (+ publish)
-            if (ALGO == ALGO_TWOSHOT && owner == p.rank) continue;  // owner reads its own grads
-            process_chunk<BT, OP_PACK>(p, c, 0);
-            __syncthreads();
-            if (tid == 0) {
-                fence_sys();
-                if (ALGO == ALGO_TWOSHOT) {
-                    st_relaxed_sys32(p.pack_flag[owner] + (size_t)c * p.N + p.rank, p.epoch);
-                } else {
-                    for (int q = 0; q < p.N; ++q)
-                        if (q != p.rank) st_relaxed_sys32(p.pack_flag[q] + (size_t)c * p.N + p.rank, p.epoch);
-                }
-            }
-        } else if (phase == 1) {  // reduce (one-shot: every chunk; two-shot: owned chunks)
-            if (ALGO == ALGO_TWOSHOT && owner != p.rank) continue;
-            if (tid == 0) {
-                for (int q = 0; q < p.N; ++q)
-                    if (q != p.rank) wait_flag(p, p.pack_flag[p.rank] + (size_t)c * p.N + q, 1);
-                s_go = !*p.abort_dev;
-            }
-            __syncthreads();
-            if (!s_go) continue;  // uniform: s_go is read after the barrier
-            if (ALGO == ALGO_TWOSHOT) {
-                process_chunk<BT, OP_RS>(p, c, 0);
+        } else if (phase == 0) {  // pack (+ publish); two-shot owners read their own grads instead
+            if (!(ALGO == ALGO_TWOSHOT && owner == p.rank)) {
+                process_chunk<BT, OP_PACK>(p, c, 0);
                 __syncthreads();
                 if (tid == 0) {
                     fence_sys();
-                    for (int q = 0; q < p.N; ++q)
-                        if (q != p.rank) st_relaxed_sys32(p.rs_flag[q] + c, p.epoch);
+                    if (ALGO == ALGO_TWOSHOT) {
+                        st_relaxed_sys32(p.pack_flag[owner] + (size_t)c * p.N + p.rank, p.epoch);
+                    } else {
+                        for (int q = 0; q < p.N; ++q)
+                            if (q != p.rank) st_relaxed_sys32(p.pack_flag[q] + (size_t)c * p.N + p.rank, p.epoch);
+                    }
                 }
-            } else {
-                process_chunk<BT, OP_RED>(p, c, 0);
             }
-        } else {  // two-shot all-gather + unpack of the chunks owned by others
-            if (owner == p.rank) continue;
+        } else if (phase == 1) {  // reduce (one-shot: every chunk; two-shot: owned chunks)
+            if (!(ALGO == ALGO_TWOSHOT && owner != p.rank)) {
+                if (tid == 0) {
+                    for (int q = 0; q < p.N; ++q)
+                        if (q != p.rank) wait_flag(p, p.pack_flag[p.rank] + (size_t)c * p.N + q, 1);
+                    s_go = !*p.abort_dev;
+                    if (p.trace) t_ready = globaltimer();
+                }
+                __syncthreads();
+                if (s_go) {  // uniform: s_go is read after the barrier
+                    if (ALGO == ALGO_TWOSHOT) {
+                        process_chunk<BT, OP_RS>(p, c, 0);
+                        __syncthreads();
+                        if (tid == 0) {
+                            fence_sys();
+                            for (int q = 0; q < p.N; ++q)
+                                if (q != p.rank) st_relaxed_sys32(p.rs_flag[q] + c, p.epoch);
+                        }
+                    } else {
+                        process_chunk<BT, OP_RED>(p, c, 0);
+                    }
+                }
+            }
+        } else if (owner != p.rank) {  // two-shot all-gather + unpack of the chunks owned by others
             if (tid == 0) {
                 wait_flag(p, p.rs_flag[p.rank] + c, 2);
                 s_go = !*p.abort_dev;
+                if (p.trace) t_ready = globaltimer();
             }
             __syncthreads();
-            if (!s_go) continue;
-            process_chunk<BT, OP_AG>(p, c, owner);
+            if (s_go) process_chunk<BT, OP_AG>(p, c, owner);
+        }
+        if (p.trace && tid == 0) {
+            uint32_t smid;
+            asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+            uint64_t *tr = p.trace + (size_t)item * 4;
+            tr[0] = t_grab;
+            tr[1] = t_ready;
+            tr[2] = globaltimer();
+            tr[3] = (uint64_t)blockIdx.x | ((uint64_t)smid << 32);
         }
     }
     if (tid == 0) {

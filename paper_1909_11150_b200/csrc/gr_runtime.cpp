@@ -11,6 +11,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
+#include <fstream>
 #include <atomic>
 #include <chrono>
 #include <cstdarg>
@@ -84,7 +86,7 @@ struct gr_ctx {
     int32_t *d_tob = nullptr, *d_gob = nullptr, *d_gbb = nullptr, *d_gbe = nullptr, *d_gnch = nullptr,
             *d_gcb = nullptr;
     int64_t *d_gel = nullptr;
-    uint32_t *d_grel = nullptr, *d_ptr_epoch = nullptr;
+    uint32_t *d_grel = nullptr;
     uint64_t *d_ptr = nullptr;
     int32_t *d_rel_ring = nullptr, *d_cum_ring = nullptr;
     int32_t *d_counters = nullptr;  // [0] work, [1] done, [2] abort
@@ -95,7 +97,6 @@ struct gr_ctx {
     gr::HostResult *h_res = nullptr;
     gr::HostError *h_err = nullptr;
     uint32_t *d_hbits = nullptr;
-    uint64_t *d_hptr = nullptr;
     gr::HostResult *d_res = nullptr;
     gr::HostError *d_err = nullptr;
     size_t res_bytes = 0;
@@ -110,10 +111,24 @@ struct gr_ctx {
     uint64_t seq = 0;
     bool step_complete = false;
     bool need_compute_fence = false;
+    std::atomic<bool> ptr_dirty{false};
     int32_t abort_flag = 0, shutdown_flag = 0;
     int sticky = 0;
     int last_algo = GR_ALGO_NONE;
     std::string err = "no error";
+
+    // tracing (GR_TRACE)
+    std::string trace_path;
+    uint64_t *d_trace = nullptr;
+    size_t trace_slot_u64 = 0;
+    struct TraceCycle {
+        int64_t cycle, step;
+        uint64_t k_start, k_pop, k_and, k_end;
+        int64_t h_enter_ns, h_launched_ns, h_seen_ns, h_done_ns;
+        int n_released, algo, nitems, slot;
+        int64_t elems;
+    };
+    std::vector<TraceCycle> trace_cycles;
 
     // stats / timing
     gr_stats stats{};
@@ -313,8 +328,6 @@ int setup_device(gr_ctx *c) {
     RC(upload(c, &c->d_gel, c->gelems));
     CK(c, cudaMalloc((void **)&c->d_grel, sizeof(uint32_t) * c->G));
     CK(c, cudaMemset(c->d_grel, 0, sizeof(uint32_t) * c->G));
-    CK(c, cudaMalloc((void **)&c->d_ptr_epoch, sizeof(uint32_t) * c->T));
-    CK(c, cudaMemset(c->d_ptr_epoch, 0, sizeof(uint32_t) * c->T));
     CK(c, cudaMalloc((void **)&c->d_ptr, sizeof(uint64_t) * c->T));
     CK(c, cudaMalloc((void **)&c->d_rel_ring, sizeof(int32_t) * GR_SLOT_RING * (size_t)c->G));
     CK(c, cudaMalloc((void **)&c->d_cum_ring, sizeof(int32_t) * GR_SLOT_RING * (size_t)(c->G + 1)));
@@ -335,7 +348,6 @@ int setup_device(gr_ctx *c) {
     CK(c, cudaHostAlloc((void **)&c->h_err, sizeof(gr::HostError), hf));
     memset((void *)c->h_err, 0, sizeof(gr::HostError));
     CK(c, cudaHostGetDevicePointer((void **)&c->d_hbits, c->h_bits, 0));
-    CK(c, cudaHostGetDevicePointer((void **)&c->d_hptr, c->h_ptr, 0));
     CK(c, cudaHostGetDevicePointer((void **)&c->d_res, (void *)c->h_res, 0));
     CK(c, cudaHostGetDevicePointer((void **)&c->d_err, (void *)c->h_err, 0));
 
@@ -345,6 +357,14 @@ int setup_device(gr_ctx *c) {
     if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &fn, cudaEnableDefault, &q) == cudaSuccess &&
         q == cudaDriverEntryPointSuccess)
         c->write_value32 = (PFN_writeValue32)fn;
+
+    if (const char *tp = getenv("GR_TRACE")) {
+        if (*tp) {
+            c->trace_path = std::string(tp) + ".rank" + std::to_string(c->rank) + ".jsonl";
+            c->trace_slot_u64 = (size_t)3 * c->C * 4;
+            CK(c, cudaMalloc((void **)&c->d_trace, sizeof(uint64_t) * c->trace_slot_u64 * GR_SLOT_RING));
+        }
+    }
 
     // data-kernel grid: every CTA co-resident (bounded by occupancy)
     for (int algo = gr::ALGO_LOCAL; algo <= gr::ALGO_TWOSHOT; ++algo) {
@@ -384,8 +404,8 @@ void free_all(gr_ctx *c) {
         if (r != c->rank && c->peer_symm[r]) cudaIpcCloseMemHandle(c->peer_symm[r]);
     cudaFree(c->symm);
     void *dptrs[] = {c->d_segs, c->d_chunks, c->d_tob, c->d_gob, c->d_gbb, c->d_gbe, c->d_gnch, c->d_gcb,
-                     c->d_gel, c->d_grel, c->d_ptr_epoch, c->d_ptr, c->d_rel_ring, c->d_cum_ring, c->d_counters,
-                     c->d_flags};
+                     c->d_gel, c->d_grel, c->d_ptr, c->d_rel_ring, c->d_cum_ring, c->d_counters,
+                     c->d_flags, c->d_trace};
     for (void *p : dptrs) cudaFree(p);
     cudaFreeHost(c->h_bits);
     cudaFreeHost(c->h_ptr);
@@ -508,6 +528,7 @@ static int mark_common(gr_ctx *c, int32_t rank, int32_t t, void *dev_ptr) {
     if (c->marked[t]) return fail(c, GR_ESTATE, "tensor %d already marked in this step", t);
     c->marked[t] = 1;
     c->h_ptr[t] = (uint64_t)(uintptr_t)dev_ptr;  // pointer first, then the flag
+    c->ptr_dirty = true;
     std::atomic_thread_fence(std::memory_order_release);
     return GR_OK;
 }
@@ -549,6 +570,7 @@ int gr_step(gr_ctx *c, int32_t *released, gr_cycle_info *info, uint32_t *global_
     if (!c || !released) return fail(c, GR_EINVAL, "null argument to gr_step");
     if (c->dry) return fail(c, GR_ESTATE, "dry context (device < 0) cannot step");
     if (c->sticky) return fail(c, GR_ESTATE, "context is in a sticky error state (%d): %s", c->sticky, c->err.c_str());
+    const auto h_enter = std::chrono::steady_clock::now();
     CK(c, cudaSetDevice(c->dev));
     const int slot = (int)(c->cycle % GR_SLOT_RING);
     if (c->ring_pending[slot]) {  // the data launch that read this slot must be done
@@ -557,6 +579,8 @@ int gr_step(gr_ctx *c, int32_t *released, gr_cycle_info *info, uint32_t *global_
     }
     uint32_t epoch;
     int32_t abort_flag, shutdown_flag;
+    bool p_inline = false;
+    uint32_t inline_bits[GR_BV_INLINE_WORDS];
     {
         std::lock_guard<std::mutex> lk(c->mu);
         if (c->step_complete) return fail(c, GR_ESTATE, "step complete: call gr_wait first");
@@ -566,6 +590,10 @@ int gr_step(gr_ctx *c, int32_t *released, gr_cycle_info *info, uint32_t *global_
             c->need_compute_fence = false;
         }
         epoch = c->epoch;
+        if (c->W <= GR_BV_INLINE_WORDS) {  // snapshot the host mark bits into the launch itself
+            p_inline = true;
+            for (int w = 0; w < c->W; ++w) inline_bits[w] = __atomic_load_n(&c->h_bits[w], __ATOMIC_ACQUIRE);
+        }
         abort_flag = c->abort_flag;
         shutdown_flag = c->shutdown_flag;
     }
@@ -573,9 +601,6 @@ int gr_step(gr_ctx *c, int32_t *released, gr_cycle_info *info, uint32_t *global_
     gr::BvParams p{};
     p.host_bits = c->d_hbits;
     p.dev_flags = c->d_flags;
-    p.host_ptr = c->d_hptr;
-    p.dev_ptr = c->d_ptr;
-    p.ptr_epoch = c->d_ptr_epoch;
     p.tensor_of_bit = c->d_tob;
     p.group_of_bit = c->d_gob;
     p.group_bit_begin = c->d_gbb;
@@ -601,6 +626,8 @@ int gr_step(gr_ctx *c, int32_t *released, gr_cycle_info *info, uint32_t *global_
     p.shutdown_flag = shutdown_flag;
     p.timeout_ns = (uint64_t)c->world.timeout_ms * 1000000ull;
     p.seq = ++c->seq;
+    p.use_inline = p_inline;
+    if (p_inline) memcpy(p.inline_bits, inline_bits, sizeof(uint32_t) * c->W);
 
     std::pair<cudaEvent_t, cudaEvent_t> evb{};
     if (c->timing) {
@@ -617,6 +644,7 @@ int gr_step(gr_ctx *c, int32_t *released, gr_cycle_info *info, uint32_t *global_
 
     // wait for the kernel's hand-off (pinned host memory), bounded
     const auto t0 = std::chrono::steady_clock::now();
+    const auto h_launched = t0;
     const auto limit = std::chrono::milliseconds(c->world.timeout_ms + 5000);
     uint64_t spins = 0;
     while (c->h_res->seq != p.seq) {
@@ -630,6 +658,9 @@ int gr_step(gr_ctx *c, int32_t *released, gr_cycle_info *info, uint32_t *global_
         }
     }
     std::atomic_thread_fence(std::memory_order_acquire);
+    const auto h_seen = std::chrono::steady_clock::now();
+    c->stats.host_wait_us += std::chrono::duration<double, std::micro>(h_seen - t0).count();
+    c->stats.bitvector_device_us += (double)(c->h_res->t_end - c->h_res->t_start) * 1e-3;
     const int status = c->h_res->status;
     const uint32_t *hA = reinterpret_cast<const uint32_t *>(c->h_res + 1);
     const int32_t *hrel = reinterpret_cast<const int32_t *>(hA + c->W);
@@ -664,6 +695,7 @@ int gr_step(gr_ctx *c, int32_t *released, gr_cycle_info *info, uint32_t *global_
         d.done_counter = c->d_counters + 1;
         d.abort_dev = c->d_counters + 2;
         d.err = c->d_err;
+        d.trace = c->d_trace ? c->d_trace + (size_t)slot * c->trace_slot_u64 : nullptr;
         d.n_released = n;
         d.total_chunks = total_chunks;
         d.rank = c->rank;
@@ -681,6 +713,10 @@ int gr_step(gr_ctx *c, int32_t *released, gr_cycle_info *info, uint32_t *global_
             evd = get_ev_pair(c);
             CK(c, cudaEventRecord(evd.first, c->s_data));
         }
+        if (c->ptr_dirty) {  // gradient pointers of this step (marked before this cycle)
+            CK(c, cudaMemcpyAsync(c->d_ptr, c->h_ptr, sizeof(uint64_t) * c->T, cudaMemcpyHostToDevice, c->s_data));
+            c->ptr_dirty = false;
+        }
         lrc = gr::launch_data(d, algo, c->buf_f16, ctas, c->s_data);
         if (lrc) return fail(c, GR_ECUDA, "data launch: %s", cudaGetErrorString((cudaError_t)lrc));
         if (c->timing) {
@@ -694,6 +730,30 @@ int gr_step(gr_ctx *c, int32_t *released, gr_cycle_info *info, uint32_t *global_
         c->stats.released_elems += rel_elems;
     }
     const int complete = c->h_res->step_complete;
+    const auto h_done = std::chrono::steady_clock::now();
+    c->stats.host_step_us += std::chrono::duration<double, std::micro>(h_done - h_enter).count();
+    if (!c->trace_path.empty()) {
+        auto ns = [](std::chrono::steady_clock::time_point t) {
+            return (int64_t)std::chrono::duration_cast<std::chrono::nanoseconds>(t.time_since_epoch()).count();
+        };
+        gr_ctx::TraceCycle tc{};
+        tc.cycle = this_cycle;
+        tc.step = c->step;
+        tc.k_start = c->h_res->t_start;
+        tc.k_pop = c->h_res->t_populated;
+        tc.k_and = c->h_res->t_anded;
+        tc.k_end = c->h_res->t_end;
+        tc.h_enter_ns = ns(h_enter);
+        tc.h_launched_ns = ns(h_launched);
+        tc.h_seen_ns = ns(h_seen);
+        tc.h_done_ns = ns(h_done);
+        tc.n_released = n;
+        tc.algo = n > 0 ? c->last_algo : 0;
+        tc.nitems = n > 0 ? total_chunks * (c->last_algo == gr::ALGO_LOCAL ? 1 : (c->last_algo == gr::ALGO_ONESHOT ? 2 : 3)) : 0;
+        tc.slot = slot;
+        tc.elems = rel_elems;
+        c->trace_cycles.push_back(tc);
+    }
     {
         std::lock_guard<std::mutex> lk(c->mu);
         if (complete) c->step_complete = true;
@@ -725,6 +785,28 @@ int gr_wait(gr_ctx *c) {
     if (c->timing) {
         int rc = collect_timing(c);
         if (rc) return rc;
+    }
+    if (!c->trace_path.empty() && !c->trace_cycles.empty()) {
+        std::ofstream f(c->trace_path, std::ios::app);
+        std::vector<uint64_t> buf;
+        for (const auto &tc : c->trace_cycles) {
+            f << "{\"cycle\":" << tc.cycle << ",\"step\":" << tc.step << ",\"rank\":" << c->rank
+              << ",\"N\":" << c->N << ",\"k\":[" << tc.k_start << "," << tc.k_pop << "," << tc.k_and << ","
+              << tc.k_end << "],\"h\":[" << tc.h_enter_ns << "," << tc.h_launched_ns << "," << tc.h_seen_ns
+              << "," << tc.h_done_ns << "],\"n_released\":" << tc.n_released << ",\"algo\":" << tc.algo
+              << ",\"elems\":" << tc.elems << ",\"items\":[";
+            if (tc.nitems > 0) {
+                buf.resize((size_t)tc.nitems * 4);
+                CK(c, cudaMemcpy(buf.data(), c->d_trace + (size_t)tc.slot * c->trace_slot_u64,
+                                 sizeof(uint64_t) * buf.size(), cudaMemcpyDeviceToHost));
+                for (int i = 0; i < tc.nitems; ++i) {
+                    if (i) f << ",";
+                    f << "[" << buf[4 * i] << "," << buf[4 * i + 1] << "," << buf[4 * i + 2] << "," << buf[4 * i + 3] << "]";
+                }
+            }
+            f << "]}\n";
+        }
+        c->trace_cycles.clear();
     }
     std::lock_guard<std::mutex> lk(c->mu);
     if (c->step_complete) {
