@@ -216,9 +216,10 @@ def main():
         if N > 1:
             dist.barrier(device_ids=[local])
 
+    batch = ctx.prepare_batch(tensor_order, [ptrs[t] for t in tensor_order])
+
     def one_step():
-        for t in tensor_order:
-            ctx.gr_mark_ready(t, ptrs[t])
+        ctx.gr_mark_ready_prepared(batch)  # all 68 tensors, reverse-layer order, one call
         rel, complete, _A, _ = ctx.gr_step()
         assert complete and len(rel) == f.G, (rel, complete)
         ctx.gr_wait()

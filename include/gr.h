@@ -123,6 +123,12 @@ int gr_init(gr_ctx **out, const gr_world *world, const gr_tensor *table, int32_t
  * this step, or the step is complete and gr_wait has not been called). */
 int gr_mark_ready(gr_ctx *ctx, int32_t rank, int32_t tensor_id, void *dev_ptr);
 
+/* gr_mark_ready_batch — LOCAL. gr_mark_ready for n tensors in one call
+ * (tensor_ids[i] with dev_ptrs[i], host arrays, borrowed for the call only).
+ * All-or-nothing validation: on error nothing is marked. */
+int gr_mark_ready_batch(gr_ctx *ctx, int32_t rank, int32_t n, const int32_t *tensor_ids,
+                        void *const *dev_ptrs);
+
 /* gr_mark_ready_async — LOCAL. Like gr_mark_ready, but readiness is
  * stream-ordered: the ready flag is written by `stream` (cudaStream_t) when
  * the work enqueued on it before this call has completed (a driver stream

@@ -65,6 +65,7 @@ def _load():
         "gr_init": ([ctypes.POINTER(p), ctypes.POINTER(GrWorld), ctypes.POINTER(GrTensor), i32, p, i32], ctypes.c_int),
         "gr_mark_ready": ([p, i32, i32, p], ctypes.c_int),
         "gr_mark_ready_async": ([p, i32, i32, p, p], ctypes.c_int),
+        "gr_mark_ready_batch": ([p, i32, i32, p, p], ctypes.c_int),
         "gr_step": ([p, p, ctypes.POINTER(GrCycleInfo), p], ctypes.c_int),
         "gr_wait": ([p], ctypes.c_int),
         "gr_set_status": ([p, i32, i32], ctypes.c_int),
@@ -83,7 +84,7 @@ def _load():
 
 
 lib = _load()
-EXPORTED = ("gr_init", "gr_mark_ready", "gr_mark_ready_async", "gr_step", "gr_wait", "gr_set_status",
+EXPORTED = ("gr_init", "gr_mark_ready", "gr_mark_ready_batch", "gr_mark_ready_async", "gr_step", "gr_wait", "gr_set_status",
             "gr_finalize", "gr_last_error", "gr_query", "gr_set_timing", "gr_reset_stats", "gr_bench_spin")
 
 
@@ -146,6 +147,23 @@ class Context:
     # -- the four calls of the method ------------------------------------------------------
     def gr_mark_ready(self, tensor_id: int, dev_ptr: int, rank: int | None = None):
         return _check(lib.gr_mark_ready(self._ctx, self.rank if rank is None else rank, tensor_id, dev_ptr), self._ctx)
+
+    def gr_mark_ready_batch(self, tensor_ids, dev_ptrs, rank: int | None = None):
+        n = len(tensor_ids)
+        ids = (ctypes.c_int32 * n)(*tensor_ids)
+        ptrs = (ctypes.c_void_p * n)(*dev_ptrs)
+        return _check(lib.gr_mark_ready_batch(self._ctx, self.rank if rank is None else rank, n,
+                                              ctypes.cast(ids, ctypes.c_void_p), ctypes.cast(ptrs, ctypes.c_void_p)),
+                      self._ctx)
+
+    def prepare_batch(self, tensor_ids, dev_ptrs):
+        """Pre-marshalled arguments for repeated gr_mark_ready_batch calls (hot loops)."""
+        n = len(tensor_ids)
+        return (n, (ctypes.c_int32 * n)(*tensor_ids), (ctypes.c_void_p * n)(*dev_ptrs))
+
+    def gr_mark_ready_prepared(self, batch, rank: int | None = None):
+        n, ids, ptrs = batch
+        return _check(lib.gr_mark_ready_batch(self._ctx, self.rank if rank is None else rank, n, ids, ptrs), self._ctx)
 
     def gr_mark_ready_async(self, tensor_id: int, dev_ptr: int, stream: int, rank: int | None = None):
         return _check(lib.gr_mark_ready_async(self._ctx, self.rank if rank is None else rank, tensor_id, dev_ptr,

@@ -53,6 +53,8 @@ struct BvParams {
     const int32_t *group_bit_end;    // device [G]
     const int32_t *group_nchunks;    // device [G]
     const int64_t *group_elems;      // device [G]
+    const int32_t *big_groups;       // device [n_big]: groups spanning > 8 bitvector words
+    int32_t n_big;
     uint32_t *group_rel_epoch;       // device [G]: epoch in which the group was released
     uint64_t *slot[GR_MAX_RANKS];    // every rank's LL bitvector slots [2][W] (own = local)
     int32_t *out_released;           // device [G]   (ring slot)
@@ -86,6 +88,13 @@ struct DataParams {
     volatile int32_t *abort_dev;       // device flag: bail out (set on timeout)
     HostError *err;                    // host-mapped
     uint64_t *trace;                   // optional [items][4]: grab, ready, done, cta|smid<<32
+    const int64_t *chunk_begin;        // [C] fusion-buffer element range of each chunk
+    const int64_t *chunk_end;          // [C]
+    int64_t stage_bytes;               // xfer kernel: bytes of one shared-memory stage
+    int32_t nstages;                   // xfer kernel: ring depth (<= 8, nstages*stage_bytes <= 208 KB)
+    int64_t slot_bytes_red;            // bytes of one peer's slot inside a stage
+    int64_t sub_red, sub_ag, sub_pack; // staged sub-tile (elements) for reduce / all-gather / pack items
+    int32_t lag1, lag2;                // queue lags (in released chunks) of reduce / all-gather items
     int32_t n_released, total_chunks;
     int32_t rank, N;
     uint32_t epoch;

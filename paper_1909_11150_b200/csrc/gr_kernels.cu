@@ -3,28 +3,27 @@
 //   bitvector_kernel  §4.1 steps 1-3 + §4.2 release rule:
 //                     ballot-populate the local bitvector from the ready flags,
 //                     publish it as LL (tag|word) 64-bit words in symmetric
-//                     memory, AND it with the N-1 peer bitvectors read over
-//                     NVLink (__reduce_and_sync across the lanes that hold the
-//                     N ranks' copies of a word), decode + release complete
-//                     groups in cache-bit order, hand the list to the host.
-//   data_kernel       fusion-buffer pack -> sum-allreduce -> x1/N
-//                     -> unpack, as ONE persistent-style kernel per cycle with a
-//                     dynamic work queue over (phase, chunk) items:
-//                       LOCAL   (N=1)  g <- fl_g(fl_b(fl_b(g) * 1))  in place, no buffer
-//                       ONESHOT        pack all; then every rank sums all N copies
-//                       TWOSHOT        pack non-owned chunks; owner reduces its
-//                                      chunks (reduce-scatter) and publishes them;
-//                                      everyone pulls the others (all-gather+unpack)
-//                     Chunk-level flags in symmetric memory pipeline the phases
-//                     across ranks; all sums run in fp32 in rank order 0..N-1, so
-//                     every rank ends with bitwise-identical gradients.
+//                     memory, AND it with the N-1 peer copies read over NVLink,
+//                     decide complete groups (thread per group, or warp per large
+//                     group with __reduce_and_sync), emit the ascending released
+//                     list and chunk prefix sums, hand the result to the host.
+//   local_kernel      N = 1: pack -> x1/N -> unpack collapsed in registers
+//                     (no peer reads the fusion buffer), HBM-bound.
+//   xfer_kernel       N > 1: fusion-buffer pack -> sum-allreduce
+//                     -> x1/N -> unpack in ONE warp-specialized kernel: a producer
+//                     lane streams peer sub-tiles into a shared-memory ring with
+//                     TMA bulk copies, consumer warps reduce / unpack. ONESHOT:
+//                     every rank sums all N copies; TWOSHOT: owner reduce-scatter
+//                     (chunk c owned by rank c mod N) + all-gather. Chunk flags in
+//                     symmetric memory pipeline the phases across ranks; sums run
+//                     in fp32 in rank order 0..N-1 on every rank, so replicas are
+//                     bitwise identical.
 //   spin_kernel       bench-only synthetic backward compute.
 //
 // Memory-model notes. Flags are pushed with a system-scope fence followed by a
-// relaxed system-scope store (release pattern); waiters use ld.acquire.sys on
-// their LOCAL pad and then bar.sync before the CTA reads peer data. Peer data
-// is read with ld.global.cg (never the non-coherent path: it changes during the
-// kernel). LL bitvector words carry their cycle tag in the upper 32 bits, so a
+// relaxed system-scope store (release pattern); the producer acquires them with
+// ld.acquire.sys on its LOCAL pad, then fence.proxy.async before the TMA reads
+// peer data. LL bitvector words carry their cycle tag in the upper 32 bits, so a
 // single 64-bit load both validates and returns the word.
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
@@ -68,6 +67,7 @@ __device__ __forceinline__ void fence_acq_rel_sys() { asm volatile("fence.acq_re
 #ifndef GR_BV_THREADS
 #define GR_BV_THREADS 512
 #endif
+#define GR_SMALL_GROUP_WORDS 8
 #ifndef GR_BV_BATCH
 #define GR_BV_BATCH 8
 #endif
@@ -77,7 +77,7 @@ constexpr int BV_BATCH = GR_BV_BATCH;
 __global__ void __launch_bounds__(BV_THREADS, 1) bitvector_kernel(BvParams p) {
     extern __shared__ uint32_t smem[];
     uint32_t *sL = smem;          // [W] local bitvector
-    uint32_t *sA = smem + p.W;    // [W] intersection
+    uint32_t *sA = smem + p.W;    // [W] intersection, then [ceil(G/32)] complete-group bits
     __shared__ int s_timeout;
     __shared__ int s_wcnt[32], s_wch[32];
     __shared__ int s_tot_cnt, s_tot_ch;
@@ -127,48 +127,27 @@ __global__ void __launch_bounds__(BV_THREADS, 1) bitvector_kernel(BvParams p) {
     __syncthreads();
     const uint64_t t_populated = globaltimer();
 
-    // ---- step 2: A = AND_r L_r. Lane group of GS lanes per word, lane rr
-    // holds rank rr's copy (own from smem, peers via NVLink LL loads). ----
-    int GS = 1;
-    while (GS < p.N) GS <<= 1;
-    const int wpw = 32 / GS;
-    const int sub = lane / GS, rr = lane % GS;
-    const unsigned gmask = (GS == 32) ? 0xffffffffu : (((1u << GS) - 1u) << (sub * GS));
+    // ---- step 2: A = AND_r L_r. One thread per word: the N-1 peer copies are
+    // LL words (tag|word) read straight from the peers' slots over NVLink, all loads issued
+    // before any is consumed; a stale tag (peer not yet in this cycle) is re-polled. ----
     const uint64_t deadline = globaltimer() + p.timeout_ns;
-    const uint64_t *peer = (rr < p.N) ? p.slot[rr] + (size_t)p.parity * p.W : nullptr;
-    const int stride = nwarps * wpw;
-    for (int base = warp * wpw; base < p.W; base += stride * BV_BATCH) {
-        uint64_t raw[BV_BATCH];
+    for (int w = tid; w < p.W; w += blockDim.x) {
+        uint64_t raw[GR_MAX_RANKS];
 #pragma unroll
-        for (int k = 0; k < BV_BATCH; ++k) {   // issue all loads first (independent)
-            const int w = base + k * stride + sub;
-            raw[k] = 0;
-            if (w < p.W && rr < p.N && rr != p.rank) raw[k] = ld_relaxed_sys64(peer + w);
-        }
-        uint32_t v[BV_BATCH];
+        for (int r = 0; r < GR_MAX_RANKS; ++r)
+            raw[r] = (r < p.N && r != p.rank) ? ld_relaxed_sys64(p.slot[r] + (size_t)p.parity * p.W + w) : 0ull;
+        uint32_t a = sL[w];
 #pragma unroll
-        for (int k = 0; k < BV_BATCH; ++k) {
-            const int w = base + k * stride + sub;
-            v[k] = 0xffffffffu;
-            if (w < p.W && rr < p.N) {
-                if (rr == p.rank) {
-                    v[k] = sL[w];
-                } else {
-                    uint64_t x = raw[k];
-                    while ((uint32_t)(x >> 32) != p.tag) {
-                        if (globaltimer() > deadline) { s_timeout = 1; break; }
-                        x = ld_relaxed_sys64(peer + w);
-                    }
-                    v[k] = (uint32_t)x;
-                }
+        for (int r = 0; r < GR_MAX_RANKS; ++r) {
+            if (r >= p.N || r == p.rank) continue;
+            uint64_t x = raw[r];
+            while ((uint32_t)(x >> 32) != p.tag) {
+                if (globaltimer() > deadline) { s_timeout = 1; break; }
+                x = ld_relaxed_sys64(p.slot[r] + (size_t)p.parity * p.W + w);
             }
+            a &= (uint32_t)x;
         }
-#pragma unroll
-        for (int k = 0; k < BV_BATCH; ++k) {
-            const int w = base + k * stride + sub;
-            const uint32_t a = __reduce_and_sync(gmask, v[k]);
-            if (rr == 0 && w < p.W) sA[w] = a;
-        }
+        sA[w] = a;
     }
     __syncthreads();
     const uint64_t t_anded = globaltimer();
@@ -180,25 +159,50 @@ __global__ void __launch_bounds__(BV_THREADS, 1) bitvector_kernel(BvParams p) {
     else if (!(sA[0] & 2u)) status = ST_SHUTDOWN;
 
     // ---- step 3 + grouping: complete groups, ascending ids ----
+    // pass 1: complete(g) = every bit of g's contiguous range set in A. Small groups: one
+    // thread each; groups spanning > GR_SMALL_GROUP_WORDS words: one warp each, the words
+    // checked lane-parallel and combined with __reduce_and_sync.
+    uint32_t *s_cbits = sA + p.W;  // [ceil(G/32)] complete-group bitmask
+    for (int i = tid; i < (p.G + 31) / 32; i += blockDim.x) s_cbits[i] = 0u;
+    __syncthreads();
+    auto word_mask = [](int w, int b0, int b1) -> uint32_t {
+        const int lo = (w == (b0 >> 5)) ? (b0 & 31) : 0;
+        const int hi = (w == ((b1 - 1) >> 5)) ? ((b1 - 1) & 31) : 31;
+        return (hi - lo == 31) ? 0xffffffffu : (((1u << (hi - lo + 1)) - 1u) << lo);
+    };
+    if (status == ST_OK) {
+        for (int g = tid; g < p.G; g += blockDim.x) {
+            if (p.group_rel_epoch[g] == p.epoch) continue;
+            const int b0 = p.group_bit_begin[g], b1 = p.group_bit_end[g];
+            if (((b1 - 1) >> 5) - (b0 >> 5) + 1 > GR_SMALL_GROUP_WORDS) continue;
+            bool ok = true;
+            for (int w = b0 >> 5; ok && w <= ((b1 - 1) >> 5); ++w) {
+                const uint32_t m = word_mask(w, b0, b1);
+                ok = (sA[w] & m) == m;
+            }
+            if (ok) atomicOr(&s_cbits[g >> 5], 1u << (g & 31));
+        }
+        for (int i = warp; i < p.n_big; i += nwarps) {
+            const int g = p.big_groups[i];
+            if (p.group_rel_epoch[g] == p.epoch) continue;  // warp-uniform
+            const int b0 = p.group_bit_begin[g], b1 = p.group_bit_end[g];
+            bool ok = true;
+            for (int w = (b0 >> 5) + lane; w <= ((b1 - 1) >> 5); w += 32) {
+                const uint32_t m = word_mask(w, b0, b1);
+                ok = ok && ((sA[w] & m) == m);
+            }
+            if (__reduce_and_sync(0xffffffffu, ok ? 1u : 0u) && lane == 0) atomicOr(&s_cbits[g >> 5], 1u << (g & 31));
+        }
+    }
+    __syncthreads();
+    // pass 2: ordered list (block-wide scan over group ids) + chunk prefix sums
     int run_base = 0, run_ch = 0;
     if (status == ST_OK) {
         for (int g0 = 0; g0 < p.G; g0 += blockDim.x) {
             const int g = g0 + tid;
-            bool rel = false;
-            int nch = 0;
-            long long el = 0;
-            if (g < p.G && p.group_rel_epoch[g] != p.epoch) {
-                const int b0 = p.group_bit_begin[g], b1 = p.group_bit_end[g];
-                bool ok = true;
-                for (int w = b0 >> 5; ok && w <= ((b1 - 1) >> 5); ++w) {
-                    const int lo = (w == (b0 >> 5)) ? (b0 & 31) : 0;
-                    const int hi = (w == ((b1 - 1) >> 5)) ? ((b1 - 1) & 31) : 31;
-                    const uint32_t mask = (hi - lo == 31) ? 0xffffffffu : (((1u << (hi - lo + 1)) - 1u) << lo);
-                    ok = (sA[w] & mask) == mask;
-                }
-                rel = ok;
-                if (rel) { nch = p.group_nchunks[g]; el = p.group_elems[g]; }
-            }
+            const bool rel = g < p.G && ((s_cbits[g >> 5] >> (g & 31)) & 1u);
+            const int nch = rel ? p.group_nchunks[g] : 0;
+            const long long el = rel ? p.group_elems[g] : 0;
             const unsigned bal = __ballot_sync(0xffffffffu, rel);
             const int wpre = __popc(bal & ((1u << lane) - 1u));
             int x = nch;  // inclusive warp scan of chunk counts
@@ -269,7 +273,7 @@ __global__ void __launch_bounds__(BV_THREADS, 1) bitvector_kernel(BvParams p) {
 }
 
 int launch_bitvector(const BvParams &p, void *stream) {
-    const size_t smem = sizeof(uint32_t) * 2 * (size_t)p.W;
+    const size_t smem = sizeof(uint32_t) * (2 * (size_t)p.W + ((size_t)p.G + 31) / 32);
     static bool attr_set = false;
     if (!attr_set) {
         cudaFuncSetAttribute(bitvector_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
@@ -282,9 +286,7 @@ int launch_bitvector(const BvParams &p, void *stream) {
 // ---------------------------------------------------------------------------------------
 // Data kernel: pack -> reduce -> x1/N -> unpack over the released chunks
 // ---------------------------------------------------------------------------------------
-constexpr int DATA_THREADS = 512;
 
-enum Op { OP_LOCAL = 0, OP_PACK = 1, OP_RS = 2, OP_RED = 3, OP_AG = 4 };
 
 template <typename BT> struct Buf;
 
@@ -326,6 +328,9 @@ template <> struct Buf<__half> {
         return __half2float(__ldcg(reinterpret_cast<const __half *>(base + idx * ES)));
     }
     __device__ static __forceinline__ float round1(float x) { return __half2float(__float2half_rn(x)); }
+    __device__ static __forceinline__ float lds1(const char *base, int64_t idx) {  // generic (shared) load
+        return __half2float(*reinterpret_cast<const __half *>(base + idx * ES));
+    }
     __device__ static __forceinline__ void store1(char *base, int64_t idx, float x) {
         *reinterpret_cast<__half *>(base + idx * ES) = __float2half_rn(x);
     }
@@ -363,6 +368,9 @@ template <> struct Buf<float> {
         return __ldcg(reinterpret_cast<const float *>(base + idx * ES));
     }
     __device__ static __forceinline__ float round1(float x) { return x; }
+    __device__ static __forceinline__ float lds1(const char *base, int64_t idx) {
+        return *reinterpret_cast<const float *>(base + idx * ES);
+    }
     __device__ static __forceinline__ void store1(char *base, int64_t idx, float x) {
         *reinterpret_cast<float *>(base + idx * ES) = x;
     }
@@ -418,126 +426,6 @@ __device__ __forceinline__ void grad_store1(char *g, int64_t idx, bool f16, floa
     else *reinterpret_cast<float *>(g + idx * 4) = x;
 }
 
-// Process one chunk with operation OP. `src_rank` is the owner for OP_AG.
-template <typename BT, int OP>
-__device__ __forceinline__ void process_chunk(const DataParams &p, int c, int src_rank) {
-    using B = Buf<BT>;
-    constexpr int UNROLL = B::UNROLL;
-    const Chunk ch = p.chunks[c];
-    const int tid = threadIdx.x;
-    const int nthr = blockDim.x;
-    for (int s = ch.seg_begin; s < ch.seg_end; ++s) {
-        const Seg sg = p.segs[s];
-        char *g = reinterpret_cast<char *>(p.dev_ptr[sg.tensor]);
-        const bool f16 = sg.grad_f16 != 0;
-        const int64_t esz = f16 ? 2 : 4;
-        const bool aligned = ((reinterpret_cast<uintptr_t>(g) + sg.tensor_off * esz) & 15) == 0;
-        const int64_t nvec = aligned ? (sg.len >> 3) : 0;
-        // ---- vector body: UNROLL vectors of 8 elements per thread, loads first ----
-        for (int64_t v0 = tid; v0 < nvec; v0 += (int64_t)nthr * UNROLL) {
-            float x[UNROLL][8];
-            bool live[UNROLL];
-            if constexpr (OP == OP_LOCAL || OP == OP_PACK) {
-                GradRaw gr[UNROLL];
-#pragma unroll
-                for (int u = 0; u < UNROLL; ++u) {
-                    const int64_t v = v0 + (int64_t)u * nthr;
-                    live[u] = v < nvec;
-                    if (live[u]) gr[u] = grad_load(g, sg.tensor_off + 8 * v, f16);
-                }
-#pragma unroll
-                for (int u = 0; u < UNROLL; ++u) {
-                    if (!live[u]) continue;
-                    const int64_t v = v0 + (int64_t)u * nthr;
-                    grad_to_f32(gr[u], f16, x[u]);
-                    typename B::Raw r = B::from_f32(x[u]);          // fl_b(g)
-                    if constexpr (OP == OP_PACK) {
-                        B::store(p.buf[p.rank], sg.buf_off + 8 * v, r);
-                    } else {  // LOCAL: single rank, sum of one, x (1/N) with N = 1
-#pragma unroll
-                        for (int i = 0; i < 8; ++i) x[u][i] = x[u][i] * p.inv_n;
-                        B::from_f32(x[u]);
-                        grad_store(g, sg.tensor_off + 8 * v, f16, x[u]);
-                    }
-                }
-            } else if constexpr (OP == OP_RS || OP == OP_RED) {
-                typename B::Raw pr[UNROLL][GR_MAX_RANKS];
-                GradRaw gr[UNROLL];
-#pragma unroll
-                for (int u = 0; u < UNROLL; ++u) {
-                    const int64_t v = v0 + (int64_t)u * nthr;
-                    live[u] = v < nvec;
-                    if (!live[u]) continue;
-                    gr[u] = grad_load(g, sg.tensor_off + 8 * v, f16);
-#pragma unroll
-                    for (int r = 0; r < GR_MAX_RANKS; ++r)
-                        if (r < p.N && r != p.rank) pr[u][r] = B::load(p.buf[r], sg.buf_off + 8 * v);
-                }
-#pragma unroll
-                for (int u = 0; u < UNROLL; ++u) {
-                    if (!live[u]) continue;
-                    const int64_t v = v0 + (int64_t)u * nthr;
-                    float acc[8];
-#pragma unroll
-                    for (int r = 0; r < GR_MAX_RANKS; ++r) {
-                        if (r >= p.N) continue;
-                        float y[8];
-                        if (r == p.rank) {
-                            grad_to_f32(gr[u], f16, y);
-                            B::from_f32(y);                           // own contribution, fl_b(g)
-                        } else {
-                            B::to_f32(pr[u][r], y);
-                        }
-#pragma unroll
-                        for (int i = 0; i < 8; ++i) acc[i] = (r == 0) ? y[i] : acc[i] + y[i];
-                    }
-#pragma unroll
-                    for (int i = 0; i < 8; ++i) acc[i] = acc[i] * p.inv_n;
-                    typename B::Raw out = B::from_f32(acc);           // fl_b(sum * 1/N)
-                    if constexpr (OP == OP_RS) B::store(p.buf[p.rank], sg.buf_off + 8 * v, out);
-                    grad_store(g, sg.tensor_off + 8 * v, f16, acc);
-                }
-            } else {  // OP_AG: pull the owner's reduced chunk, unpack
-                typename B::Raw pr[UNROLL];
-#pragma unroll
-                for (int u = 0; u < UNROLL; ++u) {
-                    const int64_t v = v0 + (int64_t)u * nthr;
-                    live[u] = v < nvec;
-                    if (live[u]) pr[u] = B::load(p.buf[src_rank], sg.buf_off + 8 * v);
-                }
-#pragma unroll
-                for (int u = 0; u < UNROLL; ++u) {
-                    if (!live[u]) continue;
-                    const int64_t v = v0 + (int64_t)u * nthr;
-                    B::to_f32(pr[u], x[u]);
-                    grad_store(g, sg.tensor_off + 8 * v, f16, x[u]);
-                }
-            }
-        }
-        // ---- scalar tail (len % 8, or an unaligned tensor) ----
-        for (int64_t e = nvec * 8 + tid; e < sg.len; e += nthr) {
-            const int64_t ti = sg.tensor_off + e, bi = sg.buf_off + e;
-            if constexpr (OP == OP_LOCAL) {
-                const float y = B::round1(B::round1(grad_load1(g, ti, f16)) * p.inv_n);
-                grad_store1(g, ti, f16, y);
-            } else if constexpr (OP == OP_PACK) {
-                B::store1(p.buf[p.rank], bi, grad_load1(g, ti, f16));
-            } else if constexpr (OP == OP_RS || OP == OP_RED) {
-                float acc = 0.f;
-                for (int r = 0; r < p.N; ++r) {
-                    const float y = (r == p.rank) ? B::round1(grad_load1(g, ti, f16)) : B::load1(p.buf[r], bi);
-                    acc = (r == 0) ? y : acc + y;
-                }
-                const float y = B::round1(acc * p.inv_n);
-                if constexpr (OP == OP_RS) B::store1(p.buf[p.rank], bi, y);
-                grad_store1(g, ti, f16, y);
-            } else {
-                grad_store1(g, ti, f16, B::load1(p.buf[src_rank], bi));
-            }
-        }
-    }
-}
-
 // chunk id of item i of the released set (binary search over the cumulative counts)
 __device__ __forceinline__ int chunk_of_item(const DataParams &p, int i) {
     int lo = 0, hi = p.n_released - 1;
@@ -548,97 +436,477 @@ __device__ __forceinline__ int chunk_of_item(const DataParams &p, int i) {
     return p.group_chunk_begin[p.released[lo]] + (i - p.cum[lo]);
 }
 
-// thread 0: wait until *flag == epoch (or abort / timeout)
-__device__ __forceinline__ void wait_flag(const DataParams &p, const uint32_t *flag, int where) {
-    if (ld_acquire_sys(flag) == p.epoch) return;
+// ---------------------------------------------------------------------------------------
+// local_kernel (N = 1): g <- fl_g(fl_b(fl_b(g) * 1/N)) in place. With one rank no peer reads
+// the fusion buffer, so pack -> reduce -> unpack collapses into one read and one write of g
+// (bit-identical to the buffered path). HBM-bound: warp-granular sub-items (no block-level
+// synchronisation), UNROLL 32-byte vectors in flight per lane, static interleaved schedule.
+// ---------------------------------------------------------------------------------------
+constexpr int LC_THREADS = 256;
+constexpr int LC_SUBS = 8;     // warp sub-items per chunk
+constexpr int LC_UNROLL = 4;
+
+template <typename BT>
+__global__ void __launch_bounds__(LC_THREADS, 3) local_kernel(DataParams p) {
+    using B = Buf<BT>;
+    const int lane = threadIdx.x & 31;
+    const int gw = blockIdx.x * (LC_THREADS / 32) + (threadIdx.x >> 5);
+    const int nw = gridDim.x * (LC_THREADS / 32);
+    const int nitems = p.total_chunks * LC_SUBS;
+    for (int it = gw; it < nitems; it += nw) {
+        const int c = chunk_of_item(p, it / LC_SUBS);
+        const int sub = it % LC_SUBS;
+        const int64_t cb = p.chunk_begin[c], ce = p.chunk_end[c];
+        const int64_t len = ((ce - cb + LC_SUBS * 8 - 1) / (LC_SUBS * 8)) * 8;  // multiple of 8
+        const int64_t sb = cb + sub * len;
+        const int64_t se = (sb + len < ce) ? sb + len : ce;
+        if (sb >= se) continue;
+        const Chunk ch = p.chunks[c];
+        for (int s = ch.seg_begin; s < ch.seg_end; ++s) {
+            const Seg sg = p.segs[s];
+            const int64_t lo = sg.buf_off > sb ? sg.buf_off : sb;
+            const int64_t hi = (sg.buf_off + sg.len) < se ? (sg.buf_off + sg.len) : se;
+            if (lo >= hi) continue;
+            char *g = reinterpret_cast<char *>(p.dev_ptr[sg.tensor]);
+            const bool f16 = sg.grad_f16 != 0;
+            const int64_t toff = sg.tensor_off + (lo - sg.buf_off);
+            const bool aligned = ((reinterpret_cast<uintptr_t>(g) + toff * (f16 ? 2 : 4)) & 15) == 0;
+            const int64_t n = hi - lo;
+            const int64_t nvec = aligned ? (n >> 3) : 0;
+            for (int64_t v0 = lane; v0 < nvec; v0 += 32 * LC_UNROLL) {
+                GradRaw gr[LC_UNROLL];
+#pragma unroll
+                for (int u = 0; u < LC_UNROLL; ++u)
+                    if (v0 + 32 * u < nvec) gr[u] = grad_load(g, toff + 8 * (v0 + 32 * u), f16);
+#pragma unroll
+                for (int u = 0; u < LC_UNROLL; ++u) {
+                    const int64_t v = v0 + 32 * u;
+                    if (v >= nvec) continue;
+                    float x[8];
+                    grad_to_f32(gr[u], f16, x);
+                    B::from_f32(x);                                   // pack: fl_b(g)
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) x[i] = x[i] * p.inv_n;  // sum of one rank, x 1/N
+                    B::from_f32(x);                                   // fl_b(. * 1/N)
+                    grad_store(g, toff + 8 * v, f16, x);              // unpack: fl_g
+                }
+            }
+            for (int64_t e = nvec * 8 + lane; e < n; e += 32) {
+                const float y = B::round1(B::round1(grad_load1(g, toff + e, f16)) * p.inv_n);
+                grad_store1(g, toff + e, f16, y);
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------------------
+// xfer_kernel: the N>1 data path, TMA-staged and warp-specialized (one CTA per SM).
+//   warp 0 / lane 0 = producer: takes work from the queue, waits for the cross-rank chunk
+//     flags, and streams the peers' fusion-buffer sub-tiles into a ring of shared-memory
+//     stages with cp.async.bulk (TMA bulk copies from NVLink peer memory, mbarrier
+//     complete_tx) — the remote latency is hidden by the ring, not by registers;
+//   warps 1..15 = consumers: pack (local LDG/STG), reduce in rank order from the staged
+//     copies + own gradients, scale, round, unpack; push chunk flags to peers.
+// Work queue: triples k = 0,1,.. each holding {PACK(k), RED/RS(k-L1), AG(k-L2)} of the
+// released chunk list; every rank takes them in the same order, so every dependency
+// (PACK(j) before RED/RS(j) before AG(j)) points backwards in every queue: no deadlock,
+// whatever subset of CTAs is resident.
+// ---------------------------------------------------------------------------------------
+constexpr int XF_THREADS = 512;
+constexpr int XF_CONS = XF_THREADS - 32;
+constexpr int XF_STAGES = 8;  // max ring depth (runtime depth: p.nstages)
+enum { K_PACK = 0, K_RED = 1, K_RS = 2, K_AG = 3, K_STOP = 4 };
+
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t *b, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *b) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(uint64_t *b, uint32_t tx) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(tx) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *b, uint32_t parity) {
+    uint32_t done = 0;
+    while (!done) {
+        asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                     : "=r"(done) : "r"(smem_u32(b)), "r"(parity) : "memory");
+    }
+}
+__device__ __forceinline__ void bulk_g2s(void *dst_smem, const void *src, uint32_t bytes, uint64_t *bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(smem_u32(dst_smem)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void consumer_sync() { asm volatile("bar.sync 1, %0;" ::"n"(XF_CONS) : "memory"); }
+
+// thread 0 of the producer: wait until *flag == epoch (or abort / timeout); false = abort
+__device__ __forceinline__ bool xf_wait_flag(const DataParams &p, const uint32_t *flag, int where) {
+    if (ld_acquire_sys(flag) == p.epoch) return true;
     const uint64_t deadline = globaltimer() + p.timeout_ns;
     while (ld_acquire_sys(flag) != p.epoch) {
-        if (*p.abort_dev) return;
+        if (*p.abort_dev) return false;
         if (globaltimer() > deadline) {
             *p.abort_dev = 1;
             p.err->where = where;
             p.err->code = ST_TIMEOUT;
-            return;
+            return false;
         }
-        __nanosleep(64);
+        __nanosleep(32);
+    }
+    return true;
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *b, uint32_t tx) {
+    asm volatile("mbarrier.expect_tx.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(tx) : "memory");
+}
+
+// One gradient piece = the overlap of a segment of chunk c with the sub-tile [sb, se).
+struct Piece {
+    char *g;          // gradient tensor base
+    int64_t lo, n;    // fusion-buffer index of the first element, element count
+    int64_t toff;     // tensor index of the first element
+    int64_t body;     // leading elements staged in shared memory by TMA (0: none)
+    bool f16;
+};
+
+constexpr int XF_MAXP = 8;  // gradient pieces described in a stage's metadata (more: slow path)
+struct XfMeta {
+    int kind, item, chunk, last;
+    int npieces;              // -1: too many pieces, consumers walk the segments themselves
+    int64_t sb, se;           // staged fusion-buffer range
+    Piece pc[XF_MAXP];
+};
+
+__device__ __forceinline__ bool piece_of(const DataParams &p, const Seg &sg, int64_t sb, int64_t se, Piece &pc) {
+    const int64_t lo = sg.buf_off > sb ? sg.buf_off : sb;
+    const int64_t hi = (sg.buf_off + sg.len) < se ? (sg.buf_off + sg.len) : se;
+    if (lo >= hi) return false;
+    pc.g = reinterpret_cast<char *>(p.dev_ptr[sg.tensor]);
+    pc.f16 = sg.grad_f16 != 0;
+    pc.lo = lo;
+    pc.n = hi - lo;
+    pc.toff = sg.tensor_off + (lo - sg.buf_off);
+    const int64_t esz = pc.f16 ? 2 : 4;
+    const bool aligned = ((reinterpret_cast<uintptr_t>(pc.g) + pc.toff * esz) & 15) == 0;
+    pc.body = aligned ? ((pc.n * esz) & ~(int64_t)15) / esz : 0;
+    return true;
+}
+
+__device__ __forceinline__ void lds_grad8(const char *src, bool f16, float (&x)[8]) {
+    GradRaw r;
+    const uint4 *q = reinterpret_cast<const uint4 *>(src);
+    r.a = q[0];
+    if (!f16) r.b = q[1];
+    grad_to_f32(r, f16, x);
+}
+__device__ __forceinline__ float lds_grad1(const char *src, int64_t e, bool f16) {
+    return f16 ? __half2float(reinterpret_cast<const __half *>(src)[e]) : reinterpret_cast<const float *>(src)[e];
+}
+
+// Consumers: one staged sub-tile [sb, se) of chunk c. Peer copies sit in slots 0..N-2 of
+// the stage (slot_bytes apart), own gradient pieces in the gradient slot (PACK/RED/RS).
+template <typename BT, int KIND>
+__device__ __forceinline__ void xf_consume(const DataParams &p, const XfMeta &m, const char *stage,
+                                           int64_t slot_bytes, const char *gslot, int ct) {
+    using B = Buf<BT>;
+    const int64_t sb = m.sb;
+    const bool slow = m.npieces < 0;
+    const Chunk ch = slow ? p.chunks[m.chunk] : Chunk{0, m.npieces};
+    for (int s = ch.seg_begin; s < ch.seg_end; ++s) {
+        Piece pc;
+        if (slow) {
+            if (!piece_of(p, p.segs[s], sb, m.se, pc)) continue;
+            pc.body = 0;  // slow path: nothing of the gradient was staged
+        } else {
+            pc = m.pc[s];
+        }
+        const int64_t esz = pc.f16 ? 2 : 4;
+        const char *gs = gslot + (pc.lo - sb) * 4;  // staged own gradient piece
+        const int64_t nvec = pc.body >> 3;
+        for (int64_t v = ct; v < nvec; v += XF_CONS) {
+            const int64_t e = 8 * v, bi = pc.lo + e, ti = pc.toff + e;
+            const int64_t so = (bi - sb) * B::ES;  // byte offset inside a peer slot
+            float acc[8];
+            if constexpr (KIND == K_PACK) {
+                lds_grad8(gs + e * esz, pc.f16, acc);
+                B::store(p.buf[p.rank], bi, B::from_f32(acc));
+                continue;
+            } else if constexpr (KIND == K_AG) {
+                B::to_f32(*reinterpret_cast<const typename B::Raw *>(stage + so), acc);
+            } else {
+                int k = 0;
+#pragma unroll
+                for (int r = 0; r < GR_MAX_RANKS; ++r) {
+                    if (r >= p.N) continue;
+                    float y[8];
+                    if (r == p.rank) {
+                        lds_grad8(gs + e * esz, pc.f16, y);
+                        B::from_f32(y);  // own contribution in buffer precision
+                    } else {
+                        B::to_f32(*reinterpret_cast<const typename B::Raw *>(stage + k * slot_bytes + so), y);
+                        ++k;
+                    }
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) acc[i] = (r == 0) ? y[i] : acc[i] + y[i];
+                }
+#pragma unroll
+                for (int i = 0; i < 8; ++i) acc[i] = acc[i] * p.inv_n;
+                typename B::Raw out = B::from_f32(acc);
+                if constexpr (KIND == K_RS) B::store(p.buf[p.rank], bi, out);
+            }
+            grad_store(pc.g, ti, pc.f16, acc);
+        }
+        for (int64_t e = nvec * 8 + ct; e < pc.n; e += XF_CONS) {  // remainder, tail, unaligned
+            const int64_t bi = pc.lo + e, ti = pc.toff + e;
+            const int64_t so = (bi - sb) * B::ES;
+            auto own = [&]() { return e < pc.body ? lds_grad1(gs, e, pc.f16) : grad_load1(pc.g, ti, pc.f16); };
+            if constexpr (KIND == K_PACK) {
+                B::store1(p.buf[p.rank], bi, own());
+                continue;
+            }
+            float y;
+            if constexpr (KIND == K_AG) {
+                y = B::lds1(stage, so / B::ES);
+            } else {
+                float a = 0.f;
+                int k = 0;
+                for (int r = 0; r < p.N; ++r) {
+                    float x;
+                    if (r == p.rank) x = B::round1(own());
+                    else { x = B::lds1(stage + k * slot_bytes, so / B::ES); ++k; }
+                    a = (r == 0) ? x : a + x;
+                }
+                y = B::round1(a * p.inv_n);
+                if constexpr (KIND == K_RS) B::store1(p.buf[p.rank], bi, y);
+            }
+            grad_store1(pc.g, ti, pc.f16, y);
+        }
     }
 }
 
+constexpr int XF_RCACHE = 512;  // released groups cached in shared memory for item -> chunk
+
 template <typename BT, int ALGO>
-__global__ void __launch_bounds__(DATA_THREADS) data_kernel(DataParams p) {
-    __shared__ int s_item, s_go;
-    const int tid = threadIdx.x;
-    const int total = p.total_chunks;
-    const int nphase = (ALGO == ALGO_LOCAL) ? 1 : (ALGO == ALGO_ONESHOT ? 2 : 3);
-    for (;;) {
-        if (tid == 0) s_item = atomicAdd(p.work_counter, 1);
-        __syncthreads();
-        const int item = s_item;
-        __syncthreads();
-        if (item >= nphase * total) break;
-        uint64_t t_grab = 0, t_ready = 0;
-        if (p.trace && tid == 0) t_grab = globaltimer();
-        const int phase = item / total;
-        const int c = chunk_of_item(p, item - phase * total);
-        const int owner = c % p.N;
-        if (ALGO == ALGO_LOCAL) {
-            process_chunk<BT, OP_LOCAL>(p, c, 0);
-        } else if (phase == 0) {  // pack (+ publish); two-shot owners read their own grads instead
-            if (!(ALGO == ALGO_TWOSHOT && owner == p.rank)) {
-                process_chunk<BT, OP_PACK>(p, c, 0);
-                __syncthreads();
-                if (tid == 0) {
-                    fence_sys();
-                    if (ALGO == ALGO_TWOSHOT) {
-                        st_relaxed_sys32(p.pack_flag[owner] + (size_t)c * p.N + p.rank, p.epoch);
-                    } else {
-                        for (int q = 0; q < p.N; ++q)
-                            if (q != p.rank) st_relaxed_sys32(p.pack_flag[q] + (size_t)c * p.N + p.rank, p.epoch);
-                    }
-                }
-            }
-        } else if (phase == 1) {  // reduce (one-shot: every chunk; two-shot: owned chunks)
-            if (!(ALGO == ALGO_TWOSHOT && owner != p.rank)) {
-                if (tid == 0) {
-                    for (int q = 0; q < p.N; ++q)
-                        if (q != p.rank) wait_flag(p, p.pack_flag[p.rank] + (size_t)c * p.N + q, 1);
-                    s_go = !*p.abort_dev;
-                    if (p.trace) t_ready = globaltimer();
-                }
-                __syncthreads();
-                if (s_go) {  // uniform: s_go is read after the barrier
-                    if (ALGO == ALGO_TWOSHOT) {
-                        process_chunk<BT, OP_RS>(p, c, 0);
-                        __syncthreads();
-                        if (tid == 0) {
-                            fence_sys();
-                            for (int q = 0; q < p.N; ++q)
-                                if (q != p.rank) st_relaxed_sys32(p.rs_flag[q] + c, p.epoch);
-                        }
-                    } else {
-                        process_chunk<BT, OP_RED>(p, c, 0);
-                    }
-                }
-            }
-        } else if (owner != p.rank) {  // two-shot all-gather + unpack of the chunks owned by others
-            if (tid == 0) {
-                wait_flag(p, p.rs_flag[p.rank] + c, 2);
-                s_go = !*p.abort_dev;
-                if (p.trace) t_ready = globaltimer();
-            }
-            __syncthreads();
-            if (s_go) process_chunk<BT, OP_AG>(p, c, owner);
+__global__ void __launch_bounds__(XF_THREADS, 1) xfer_kernel(DataParams p) {
+    using B = Buf<BT>;
+    extern __shared__ __align__(1024) char xsm[];
+    __shared__ __align__(8) uint64_t full[XF_STAGES], empty[XF_STAGES];
+    __shared__ XfMeta meta[XF_STAGES];
+    __shared__ int s_cum[XF_RCACHE], s_cb[XF_RCACHE];
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int64_t stage_bytes = p.stage_bytes;
+    const int64_t gslot_off = p.slot_bytes_red * (p.N - 1);  // gradient slot inside a RED/RS stage
+    if (tid == 0) {
+        for (int s = 0; s < XF_STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], XF_CONS / 32);
         }
-        if (p.trace && tid == 0) {
-            uint32_t smid;
-            asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
-            uint64_t *tr = p.trace + (size_t)item * 4;
-            tr[0] = t_grab;
-            tr[1] = t_ready;
-            tr[2] = globaltimer();
-            tr[3] = (uint64_t)blockIdx.x | ((uint64_t)smid << 32);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+    const int nst = p.nstages;
+    const bool cached = p.n_released <= XF_RCACHE;
+    if (cached)
+        for (int j = tid; j < p.n_released; j += blockDim.x) {
+            s_cum[j] = p.cum[j];
+            s_cb[j] = p.group_chunk_begin[p.released[j]];
+        }
+    __syncthreads();
+    auto chunk_of = [&](int i) -> int {
+        if (!cached) return chunk_of_item(p, i);
+        int lo = 0, hi = p.n_released - 1;
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (s_cum[mid] <= i) lo = mid; else hi = mid - 1;
+        }
+        return s_cb[lo] + (i - s_cum[lo]);
+    };
+    const int total = p.total_chunks;
+    const int nk = total + p.lag2;  // queue triples
+    if (warp == 0) {
+        // ---------------- producer warp: lane 0 owns the queue, barriers and flag waits;
+        // the 32 lanes describe / stage the chunk's gradient pieces and issue the peer
+        // TMA copies in parallel (no serial chain of dependent global loads per stage).
+        int stage = 0;
+        uint32_t ph = 1;  // empty barriers start "free"
+        const unsigned FULL = 0xffffffffu;
+        // stream chunk c as sub-tiles of `sub` elements. src: 0 none (PACK), 1 every peer
+        // (RED/RS), 2 the owner (AG); grads: stage own gradient pieces (PACK/RED/RS)
+        auto produce = [&](int kind, int item, int c, int64_t sub, int src, int owner, bool grads) {
+            const Chunk ch = p.chunks[c];
+            const int nseg = ch.seg_end - ch.seg_begin;
+            Seg sg{};
+            char *gp = nullptr;
+            const bool have = lane < nseg;
+            if (have) {
+                sg = p.segs[ch.seg_begin + lane];
+                gp = reinterpret_cast<char *>(p.dev_ptr[sg.tensor]);
+            }
+            const int64_t cb = p.chunk_begin[c], ce = p.chunk_end[c];
+            const int nsub = (int)((ce - cb + sub - 1) / sub);
+            for (int t = 0; t < nsub; ++t) {
+                const int64_t sb = cb + t * sub, se = (sb + sub < ce) ? sb + sub : ce;
+                if (lane == 0) mbar_wait(&empty[stage], ph);
+                __syncwarp();
+                XfMeta &m = meta[stage];
+                char *dst = xsm + (size_t)stage * stage_bytes;
+                Piece pc{};
+                bool has = false;
+                if (have) {
+                    const int64_t lo = sg.buf_off > sb ? sg.buf_off : sb;
+                    const int64_t hi = (sg.buf_off + sg.len) < se ? (sg.buf_off + sg.len) : se;
+                    if (lo < hi) {
+                        has = true;
+                        pc.g = gp;
+                        pc.f16 = sg.grad_f16 != 0;
+                        pc.lo = lo;
+                        pc.n = hi - lo;
+                        pc.toff = sg.tensor_off + (lo - sg.buf_off);
+                        const int64_t esz = pc.f16 ? 2 : 4;
+                        const bool al = ((reinterpret_cast<uintptr_t>(gp) + pc.toff * esz) & 15) == 0;
+                        pc.body = al ? ((pc.n * esz) & ~(int64_t)15) / esz : 0;
+                    }
+                }
+                const unsigned bal = __ballot_sync(FULL, has);
+                const int np = __popc(bal);
+                const bool fast = nseg <= 32 && np <= XF_MAXP;  // else: consumers walk segments, no staged grads
+                if (!(grads && fast)) pc.body = 0;
+                if (has && fast) m.pc[__popc(bal & ((1u << lane) - 1u))] = pc;
+                if (lane == 0) {
+                    m.kind = kind;
+                    m.item = item;
+                    m.chunk = c;
+                    m.last = t == nsub - 1;
+                    m.sb = sb;
+                    m.se = se;
+                    m.npieces = fast ? np : -1;
+                }
+                uint64_t *bar = &full[stage];
+                if (has && pc.body > 0) {  // own gradient piece -> gradient slot
+                    const int64_t esz = pc.f16 ? 2 : 4;
+                    const char *gs = dst + (src == 1 ? gslot_off : 0) + (pc.lo - sb) * 4;
+                    mbar_expect_tx(bar, (uint32_t)(pc.body * esz));
+                    bulk_g2s(const_cast<char *>(gs), pc.g + pc.toff * esz, (uint32_t)(pc.body * esz), bar);
+                }
+                if (src) {  // peer copies: lane r fetches rank r's sub-tile
+                    const uint32_t bytes = (uint32_t)(((se - sb) * B::ES + 15) & ~(int64_t)15);
+                    const bool mine = src == 1 ? (lane < p.N && lane != p.rank) : (lane == owner);
+                    if (mine) {
+                        const int slot = (src == 1) ? (lane < p.rank ? lane : lane - 1) : 0;
+                        mbar_expect_tx(bar, bytes);
+                        bulk_g2s(dst + (size_t)slot * p.slot_bytes_red, p.buf[lane] + sb * B::ES, bytes, bar);
+                    }
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(bar);  // release: meta + expected bytes registered
+                if (++stage == nst) { stage = 0; ph ^= 1; }
+            }
+        };
+        // lane 0: wait for all flags, broadcast the verdict, order the TMA reads after it
+        auto wait_flags = [&](const uint32_t *base, int stride, int count, int skip, int where) -> bool {
+            int ok = 1;
+            if (lane == 0)
+                for (int q = 0; q < count && ok; ++q)
+                    if (q != skip) ok = xf_wait_flag(p, base + (size_t)q * stride, where);
+            ok = __shfl_sync(FULL, ok, 0);
+            asm volatile("fence.proxy.async.global;" ::: "memory");
+            return ok != 0;
+        };
+        int kq = 0;
+        if (lane == 0) kq = atomicAdd(p.work_counter, 1);
+        bool ok = true;
+        for (;;) {
+            const int k = __shfl_sync(FULL, kq, 0);
+            if (k >= nk || !ok) break;
+            if (lane == 0) kq = atomicAdd(p.work_counter, 1);  // prefetch the next triple
+            // PACK(k): own gradients (TMA) -> fusion buffer (consumers), flag -> peers
+            if (k < total) {
+                const int c = chunk_of(k);
+                if (!(ALGO == ALGO_TWOSHOT && c % p.N == p.rank)) {
+                    if (p.trace && lane == 0) { const uint64_t t = globaltimer(); p.trace[(size_t)k * 4] = t; p.trace[(size_t)k * 4 + 1] = t; }
+                    produce(K_PACK, k, c, p.sub_pack, 0, -1, true);
+                }
+            }
+            // RED(k-L1) (one-shot, every chunk) / RS(k-L1) (two-shot, owned chunks)
+            const int i1 = k - p.lag1;
+            if (i1 >= 0 && i1 < total) {
+                const int c = chunk_of(i1);
+                if (ALGO == ALGO_ONESHOT || c % p.N == p.rank) {
+                    uint64_t *tr = p.trace ? p.trace + ((size_t)total + i1) * 4 : nullptr;
+                    if (tr && lane == 0) tr[0] = globaltimer();
+                    // one-shot also waits for its own PACK(c): RED overwrites g after PACK read it
+                    ok = wait_flags(p.pack_flag[p.rank] + (size_t)c * p.N, 1, p.N, ALGO == ALGO_ONESHOT ? -1 : p.rank, 1);
+                    if (!ok) break;
+                    if (tr && lane == 0) tr[1] = globaltimer();
+                    produce(ALGO == ALGO_ONESHOT ? K_RED : K_RS, total + i1, c, p.sub_red, 1, -1, true);
+                }
+            }
+            // AG(k-L2) (two-shot): pull the owner's reduced chunk
+            if (ALGO == ALGO_TWOSHOT) {
+                const int i2 = k - p.lag2;
+                if (i2 >= 0 && i2 < total) {
+                    const int c = chunk_of(i2);
+                    const int owner = c % p.N;
+                    if (owner != p.rank) {
+                        uint64_t *tr = p.trace ? p.trace + ((size_t)2 * total + i2) * 4 : nullptr;
+                        if (tr && lane == 0) tr[0] = globaltimer();
+                        ok = wait_flags(p.rs_flag[p.rank] + c, 0, 1, -1, 2);
+                        if (!ok) break;
+                        if (tr && lane == 0) tr[1] = globaltimer();
+                        produce(K_AG, 2 * total + i2, c, p.sub_ag, 2, owner, false);
+                    }
+                }
+            }
+        }
+        if (lane == 0) {  // stop message
+            mbar_wait(&empty[stage], ph);
+            meta[stage].kind = K_STOP;
+            mbar_arrive(&full[stage]);
+        }
+    } else {
+        const int ct = tid - 32;  // consumer thread index
+        int stage = 0;
+        uint32_t ph = 0;
+        for (;;) {
+            mbar_wait(&full[stage], ph);
+            const XfMeta &m = meta[stage];
+            const int kind = m.kind;
+            if (kind == K_STOP) break;
+            const int item = m.item, c = m.chunk, last = m.last;
+            const char *st = xsm + (size_t)stage * stage_bytes;
+            if (kind == K_PACK) xf_consume<BT, K_PACK>(p, m, st, 0, st, ct);
+            else if (kind == K_RED) xf_consume<BT, K_RED>(p, m, st, p.slot_bytes_red, st + gslot_off, ct);
+            else if (kind == K_RS) xf_consume<BT, K_RS>(p, m, st, p.slot_bytes_red, st + gslot_off, ct);
+            else xf_consume<BT, K_AG>(p, m, st, 0, st, ct);
+            // the stage is free once every consumer warp has read it
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[stage]);
+            if (last && (kind == K_PACK || kind == K_RS)) {  // chunk done: publish its flag
+                consumer_sync();
+                if (ct == 0) {
+                    fence_sys();
+                    if (kind == K_RS) {
+                        for (int q = 0; q < p.N; ++q)
+                            if (q != p.rank) st_relaxed_sys32(p.rs_flag[q] + c, p.epoch);
+                    } else if (ALGO == ALGO_TWOSHOT) {
+                        st_relaxed_sys32(p.pack_flag[c % p.N] + (size_t)c * p.N + p.rank, p.epoch);
+                    } else {  // every rank, this one included: RED(c) must not overwrite g before PACK(c) read it
+                        for (int q = 0; q < p.N; ++q) st_relaxed_sys32(p.pack_flag[q] + (size_t)c * p.N + p.rank, p.epoch);
+                    }
+                }
+            }
+            if (p.trace && last && ct == 0) {
+                uint32_t smid;
+                asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+                p.trace[(size_t)item * 4 + 2] = globaltimer();
+                p.trace[(size_t)item * 4 + 3] = (uint64_t)blockIdx.x | ((uint64_t)smid << 32);
+            }
+            if (++stage == nst) { stage = 0; ph ^= 1; }
         }
     }
+    __syncthreads();
     if (tid == 0) {
         __threadfence();
         if (atomicAdd(p.done_counter, 1) == (int)gridDim.x - 1) {
@@ -651,10 +919,17 @@ __global__ void __launch_bounds__(DATA_THREADS) data_kernel(DataParams p) {
 
 template <typename BT>
 static int launch_data_t(const DataParams &p, int algo, int ctas, cudaStream_t s) {
+    const size_t xsmem = (size_t)p.nstages * p.stage_bytes;
+    static bool attr_set = false;
+    if (!attr_set) {
+        cudaFuncSetAttribute(xfer_kernel<BT, ALGO_ONESHOT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 208 * 1024);
+        cudaFuncSetAttribute(xfer_kernel<BT, ALGO_TWOSHOT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 208 * 1024);
+        attr_set = true;
+    }
     switch (algo) {
-        case ALGO_LOCAL: data_kernel<BT, ALGO_LOCAL><<<ctas, DATA_THREADS, 0, s>>>(p); break;
-        case ALGO_ONESHOT: data_kernel<BT, ALGO_ONESHOT><<<ctas, DATA_THREADS, 0, s>>>(p); break;
-        default: data_kernel<BT, ALGO_TWOSHOT><<<ctas, DATA_THREADS, 0, s>>>(p); break;
+        case ALGO_LOCAL: local_kernel<BT><<<ctas, LC_THREADS, 0, s>>>(p); break;
+        case ALGO_ONESHOT: xfer_kernel<BT, ALGO_ONESHOT><<<ctas, XF_THREADS, xsmem, s>>>(p); break;
+        default: xfer_kernel<BT, ALGO_TWOSHOT><<<ctas, XF_THREADS, xsmem, s>>>(p); break;
     }
     return (int)cudaGetLastError();
 }
@@ -665,14 +940,9 @@ int launch_data(const DataParams &p, int algo, int buffer_f16, int ctas, void *s
 }
 
 template <typename BT>
-static int max_ctas_t(int algo, int *out) {
+static int max_ctas_t(int *out) {
     int per_sm = 0, dev = 0, sms = 0;
-    cudaError_t e;
-    switch (algo) {
-        case ALGO_LOCAL: e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, data_kernel<BT, ALGO_LOCAL>, DATA_THREADS, 0); break;
-        case ALGO_ONESHOT: e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, data_kernel<BT, ALGO_ONESHOT>, DATA_THREADS, 0); break;
-        default: e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, data_kernel<BT, ALGO_TWOSHOT>, DATA_THREADS, 0); break;
-    }
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, local_kernel<BT>, LC_THREADS, 0);
     if (e != cudaSuccess) return (int)e;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -681,7 +951,8 @@ static int max_ctas_t(int algo, int *out) {
 }
 
 int data_kernel_max_ctas(int algo, int buffer_f16, int *out) {
-    return buffer_f16 ? max_ctas_t<__half>(algo, out) : max_ctas_t<float>(algo, out);
+    (void)algo;
+    return buffer_f16 ? max_ctas_t<__half>(out) : max_ctas_t<float>(out);
 }
 
 // ---------------------------------------------------------------------------------------

@@ -66,8 +66,10 @@ struct gr_ctx {
     std::vector<int32_t> grad_f16, group_of, bit_of, tensor_of_bit, group_of_bit;
     std::vector<int32_t> gbit_begin, gbit_end, gnchunks, gchunk_begin;
     std::vector<int64_t> buf_off, gelems;
+    std::vector<int32_t> big_groups;
     std::vector<Seg> segs;
     std::vector<Chunk> chunks;
+    std::vector<int64_t> chunk_begin, chunk_end;
     int64_t buf_elems = 0;
     int32_t C = 0;
 
@@ -83,9 +85,11 @@ struct gr_ctx {
     char *peer_symm[GR_MAX_RANKS] = {};
     Seg *d_segs = nullptr;
     Chunk *d_chunks = nullptr;
+    int64_t *d_cbeg = nullptr, *d_cend = nullptr;
     int32_t *d_tob = nullptr, *d_gob = nullptr, *d_gbb = nullptr, *d_gbe = nullptr, *d_gnch = nullptr,
             *d_gcb = nullptr;
     int64_t *d_gel = nullptr;
+    int32_t *d_big = nullptr;
     uint32_t *d_grel = nullptr;
     uint64_t *d_ptr = nullptr;
     int32_t *d_rel_ring = nullptr, *d_cum_ring = nullptr;
@@ -102,6 +106,8 @@ struct gr_ctx {
     size_t res_bytes = 0;
     PFN_writeValue32 write_value32 = nullptr;
     int data_ctas[4] = {0, 0, 0, 0};
+    int lag1 = 0, lag2 = 0;  // GR_LAG1 / GR_LAG2 overrides (tuning)
+    int nstages = 4, stage_kb = 48;  // GR_STAGES / GR_STAGE_KB overrides (tuning)
 
     // step / cycle state
     std::mutex mu;
@@ -209,6 +215,9 @@ int build_layouts(gr_ctx *c, const gr_tensor *table, const int32_t *group_of) {
         c->gbit_end[g] = std::max(c->gbit_end[g], b + 1);
     }
 
+    for (int32_t g = 0; g < G; ++g)
+        if (((c->gbit_end[g] - 1) >> 5) - (c->gbit_begin[g] >> 5) + 1 > 8) c->big_groups.push_back(g);
+
     // static fusion layout: same order, every tensor 8-element (16 B at fp16) aligned
     c->buf_off.assign(T, 0);
     c->gelems.assign(G, 0);
@@ -230,6 +239,8 @@ int build_layouts(gr_ctx *c, const gr_tensor *table, const int32_t *group_of) {
     c->gnchunks.assign(G, 0);
     c->segs.clear();
     c->chunks.clear();
+    c->chunk_begin.clear();
+    c->chunk_end.clear();
     int32_t pos = 0;
     for (int32_t g = 0; g < G; ++g) {
         c->gchunk_begin[g] = (int32_t)c->chunks.size();
@@ -254,6 +265,8 @@ int build_layouts(gr_ctx *c, const gr_tensor *table, const int32_t *group_of) {
             }
             ch.seg_end = (int32_t)c->segs.size();
             c->chunks.push_back(ch);
+            c->chunk_begin.push_back(cb);
+            c->chunk_end.push_back(ce);
         }
         c->gnchunks[g] = (int32_t)c->chunks.size() - c->gchunk_begin[g];
     }
@@ -319,6 +332,8 @@ int setup_device(gr_ctx *c) {
 
     RC(upload(c, &c->d_segs, c->segs));
     RC(upload(c, &c->d_chunks, c->chunks));
+    RC(upload(c, &c->d_cbeg, c->chunk_begin));
+    RC(upload(c, &c->d_cend, c->chunk_end));
     RC(upload(c, &c->d_tob, c->tensor_of_bit));
     RC(upload(c, &c->d_gob, c->group_of_bit));
     RC(upload(c, &c->d_gbb, c->gbit_begin));
@@ -326,6 +341,7 @@ int setup_device(gr_ctx *c) {
     RC(upload(c, &c->d_gnch, c->gnchunks));
     RC(upload(c, &c->d_gcb, c->gchunk_begin));
     RC(upload(c, &c->d_gel, c->gelems));
+    RC(upload(c, &c->d_big, c->big_groups));
     CK(c, cudaMalloc((void **)&c->d_grel, sizeof(uint32_t) * c->G));
     CK(c, cudaMemset(c->d_grel, 0, sizeof(uint32_t) * c->G));
     CK(c, cudaMalloc((void **)&c->d_ptr, sizeof(uint64_t) * c->T));
@@ -358,6 +374,12 @@ int setup_device(gr_ctx *c) {
         q == cudaDriverEntryPointSuccess)
         c->write_value32 = (PFN_writeValue32)fn;
 
+    if (const char *os = getenv("GR_ONESHOT_MAX_BYTES")) c->one_shot_max_bytes = atoll(os);  // tuning
+    if (const char *l1 = getenv("GR_LAG1")) c->lag1 = atoi(l1);
+    if (const char *ns = getenv("GR_STAGES")) c->nstages = std::max(2, std::min(8, atoi(ns)));
+    if (const char *sk = getenv("GR_STAGE_KB")) c->stage_kb = std::max(8, atoi(sk));
+    if (c->nstages * c->stage_kb > 208) c->stage_kb = 208 / c->nstages / 16 * 16;
+    if (const char *l2 = getenv("GR_LAG2")) c->lag2 = atoi(l2);
     if (const char *tp = getenv("GR_TRACE")) {
         if (*tp) {
             c->trace_path = std::string(tp) + ".rank" + std::to_string(c->rank) + ".jsonl";
@@ -367,9 +389,11 @@ int setup_device(gr_ctx *c) {
     }
 
     // data-kernel grid: every CTA co-resident (bounded by occupancy)
+    int sms = 0;
+    CK(c, cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->dev));
     for (int algo = gr::ALGO_LOCAL; algo <= gr::ALGO_TWOSHOT; ++algo) {
-        int mx = 0;
-        int rc = gr::data_kernel_max_ctas(algo, c->buf_f16, &mx);
+        int mx = sms;  // xfer kernel: one CTA per SM (shared-memory stage ring)
+        int rc = algo == gr::ALGO_LOCAL ? gr::data_kernel_max_ctas(algo, c->buf_f16, &mx) : 0;
         if (rc != 0) return fail(c, GR_ECUDA, "occupancy query failed: %s", cudaGetErrorString((cudaError_t)rc));
         int want = c->world.comm_ctas > 0 ? c->world.comm_ctas : mx;
         c->data_ctas[algo] = std::max(1, std::min(want, mx));
@@ -403,8 +427,8 @@ void free_all(gr_ctx *c) {
     for (int r = 0; r < c->N; ++r)
         if (r != c->rank && c->peer_symm[r]) cudaIpcCloseMemHandle(c->peer_symm[r]);
     cudaFree(c->symm);
-    void *dptrs[] = {c->d_segs, c->d_chunks, c->d_tob, c->d_gob, c->d_gbb, c->d_gbe, c->d_gnch, c->d_gcb,
-                     c->d_gel, c->d_grel, c->d_ptr, c->d_rel_ring, c->d_cum_ring, c->d_counters,
+    void *dptrs[] = {c->d_segs, c->d_chunks, c->d_cbeg, c->d_cend, c->d_tob, c->d_gob, c->d_gbb, c->d_gbe, c->d_gnch, c->d_gcb,
+                     c->d_gel, c->d_big, c->d_grel, c->d_ptr, c->d_rel_ring, c->d_cum_ring, c->d_counters,
                      c->d_flags, c->d_trace};
     for (void *p : dptrs) cudaFree(p);
     cudaFreeHost(c->h_bits);
@@ -527,8 +551,10 @@ static int mark_common(gr_ctx *c, int32_t rank, int32_t t, void *dev_ptr) {
     if (c->step_complete) return fail(c, GR_ESTATE, "step complete: call gr_wait before marking again");
     if (c->marked[t]) return fail(c, GR_ESTATE, "tensor %d already marked in this step", t);
     c->marked[t] = 1;
-    c->h_ptr[t] = (uint64_t)(uintptr_t)dev_ptr;  // pointer first, then the flag
-    c->ptr_dirty = true;
+    if (c->h_ptr[t] != (uint64_t)(uintptr_t)dev_ptr) {  // pointer first, then the flag
+        c->h_ptr[t] = (uint64_t)(uintptr_t)dev_ptr;
+        c->ptr_dirty = true;                            // re-upload only when it changed
+    }
     std::atomic_thread_fence(std::memory_order_release);
     return GR_OK;
 }
@@ -541,6 +567,32 @@ int gr_mark_ready(gr_ctx *c, int32_t rank, int32_t t, void *dev_ptr) {
     c->need_compute_fence = true;
     const int32_t b = c->bit_of[t];
     __atomic_fetch_or(&c->h_bits[b >> 5], 1u << (b & 31), __ATOMIC_RELEASE);
+    return GR_OK;
+}
+
+int gr_mark_ready_batch(gr_ctx *c, int32_t rank, int32_t n, const int32_t *ids, void *const *ptrs) {
+    if (!c) return GR_EINVAL;
+    if (n < 0 || (n > 0 && (!ids || !ptrs))) return fail(c, GR_EINVAL, "bad batch");
+    std::lock_guard<std::mutex> lk(c->mu);
+    for (int32_t i = 0; i < n; ++i) {  // validate everything first: all-or-nothing
+        const int32_t t = ids[i];
+        if (c->dry) return fail(c, GR_ESTATE, "dry context (device < 0) cannot mark");
+        if (c->sticky) return fail(c, GR_ESTATE, "context is in a sticky error state (%d)", c->sticky);
+        if (rank != c->rank) return fail(c, GR_EINVAL, "rank %d != world.rank %d", rank, c->rank);
+        if (t < 0 || t >= c->T) return fail(c, GR_EINVAL, "tensor id %d out of range", t);
+        if (!ptrs[i]) return fail(c, GR_EINVAL, "null dev_ptr for tensor %d", t);
+        if (c->step_complete) return fail(c, GR_ESTATE, "step complete: call gr_wait before marking again");
+        if (c->marked[t]) return fail(c, GR_ESTATE, "tensor %d already marked in this step", t);
+        for (int32_t j = 0; j < i; ++j)
+            if (ids[j] == t) return fail(c, GR_ESTATE, "tensor %d twice in one batch", t);
+    }
+    for (int32_t i = 0; i < n; ++i) {
+        int rc = mark_common(c, rank, ids[i], ptrs[i]);
+        if (rc) return rc;
+        const int32_t b = c->bit_of[ids[i]];
+        __atomic_fetch_or(&c->h_bits[b >> 5], 1u << (b & 31), __ATOMIC_RELEASE);
+    }
+    if (n > 0) c->need_compute_fence = true;
     return GR_OK;
 }
 
@@ -607,6 +659,8 @@ int gr_step(gr_ctx *c, int32_t *released, gr_cycle_info *info, uint32_t *global_
     p.group_bit_end = c->d_gbe;
     p.group_nchunks = c->d_gnch;
     p.group_elems = c->d_gel;
+    p.big_groups = c->d_big;
+    p.n_big = (int32_t)c->big_groups.size();
     p.group_rel_epoch = c->d_grel;
     for (int r = 0; r < c->N; ++r) p.slot[r] = reinterpret_cast<uint64_t *>(c->peer_symm[r] + c->off_slot);
     p.out_released = c->d_rel_ring + (size_t)slot * c->G;
@@ -696,6 +750,21 @@ int gr_step(gr_ctx *c, int32_t *released, gr_cycle_info *info, uint32_t *global_
         d.abort_dev = c->d_counters + 2;
         d.err = c->d_err;
         d.trace = c->d_trace ? c->d_trace + (size_t)slot * c->trace_slot_u64 : nullptr;
+        d.chunk_begin = c->d_cbeg;
+        d.chunk_end = c->d_cend;
+        {
+            const int64_t es = c->buf_f16 ? 2 : 4;
+            const int64_t stage = c->stage_kb * 1024;
+            d.stage_bytes = stage;
+            d.nstages = c->nstages;
+            // RED/RS stage: N-1 peer slots (buffer precision) + one fp32-spaced gradient slot
+            int64_t sr = c->N > 1 ? stage / ((c->N - 1) * es + 4) / 256 * 256 : 256;
+            sr = std::max<int64_t>(256, std::min<int64_t>(sr, c->chunk_elems));
+            d.sub_red = sr;
+            d.slot_bytes_red = sr * es;
+            d.sub_pack = std::max<int64_t>(256, std::min<int64_t>(stage / 4 / 256 * 256, c->chunk_elems));
+            d.sub_ag = std::max<int64_t>(256, std::min<int64_t>(stage / es / 256 * 256, c->chunk_elems));
+        }
         d.n_released = n;
         d.total_chunks = total_chunks;
         d.rank = c->rank;
@@ -708,6 +777,9 @@ int gr_step(gr_ctx *c, int32_t *released, gr_cycle_info *info, uint32_t *global_
         if (c->N > 1) algo = msg_bytes <= c->one_shot_max_bytes ? gr::ALGO_ONESHOT : gr::ALGO_TWOSHOT;
         const int nitems = total_chunks * (algo == gr::ALGO_LOCAL ? 1 : (algo == gr::ALGO_ONESHOT ? 2 : 3));
         const int ctas = std::max(1, std::min(c->data_ctas[algo], nitems));
+        d.lag1 = c->lag1 > 0 ? c->lag1 : 2 * ctas;
+        d.lag2 = c->lag2 > 0 ? c->lag2 : 4 * ctas;
+        if (algo == gr::ALGO_ONESHOT) d.lag2 = d.lag1;
         std::pair<cudaEvent_t, cudaEvent_t> evd{};
         if (c->timing) {
             evd = get_ev_pair(c);
@@ -717,6 +789,7 @@ int gr_step(gr_ctx *c, int32_t *released, gr_cycle_info *info, uint32_t *global_
             CK(c, cudaMemcpyAsync(c->d_ptr, c->h_ptr, sizeof(uint64_t) * c->T, cudaMemcpyHostToDevice, c->s_data));
             c->ptr_dirty = false;
         }
+        if (d.trace) CK(c, cudaMemsetAsync(d.trace, 0, sizeof(uint64_t) * 4 * (size_t)nitems, c->s_data));
         lrc = gr::launch_data(d, algo, c->buf_f16, ctas, c->s_data);
         if (lrc) return fail(c, GR_ECUDA, "data launch: %s", cudaGetErrorString((cudaError_t)lrc));
         if (c->timing) {

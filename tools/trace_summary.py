@@ -38,6 +38,8 @@ def main():
             if not it:
                 continue
             live = [x for x in it if x[0]]
+            if not live:
+                continue
             t0 = min(x[0] for x in live)
             t1 = max(x[2] for x in live)
             ctas = len({x[3] & 0xffffffff for x in live})
@@ -47,7 +49,7 @@ def main():
             nph = {1: 1, 2: 2, 3: 3}.get(r["algo"], 1)
             per = n // nph
             for ph in range(nph):
-                seg = [x for x in it[ph * per:(ph + 1) * per] if x[0]]
+                seg = [x for x in it[ph * per:(ph + 1) * per] if x[0] and x[2]]
                 if not seg:
                     continue
                 dur = [(x[2] - x[0]) / 1e3 for x in seg]
