@@ -275,13 +275,13 @@ def main():
         roof = {"bound": "hbm", "achieved": round(alg_bytes / (kern_ms * 1e-3) / 1e9, 1),
                 "peak": hbm if hbm else 6650.0, "unit": "GB/s",
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs" if hbm else "B200_PROFILING.md fallback",
-                "kernel": "data_kernel<half,LOCAL>", "algorithmic_bytes_per_launch": alg_bytes,
+                "kernel": f"local_kernel<{'half' if buf16 else 'float'}>", "algorithmic_bytes_per_launch": alg_bytes,
                 "kernel_ms": round(kern_ms, 4)}
     else:
         alg_bytes = int(2 * (N - 1) / N * S)  # bytes that must cross NVLink per direction per rank
         roof = {"bound": "nvlink", "achieved": round(alg_bytes / (kern_ms * 1e-3) / 1e9, 1), "peak": 770.0,
                 "unit": "GB/s", "peak_source": "B200_PROFILING.md measured peer copy per direction (900 nominal)",
-                "kernel": f"data_kernel<half,{'TWOSHOT' if algo == 3 else 'ONESHOT'}>",
+                "kernel": f"xfer_kernel<{'half' if buf16 else 'float'},{'TWOSHOT' if algo == 3 else 'ONESHOT'}>",
                 "algorithmic_bytes_per_launch": alg_bytes, "kernel_ms": round(kern_ms, 4)}
     roof["frac"] = round(roof["achieved"] / roof["peak"], 4)
     roof["traffic"] = None

@@ -107,7 +107,7 @@ struct gr_ctx {
     PFN_writeValue32 write_value32 = nullptr;
     int data_ctas[4] = {0, 0, 0, 0};
     int lag1 = 0, lag2 = 0;  // GR_LAG1 / GR_LAG2 overrides (tuning)
-    int nstages = 4, stage_kb = 48;  // GR_STAGES / GR_STAGE_KB overrides (tuning)
+    int nstages = 6, stage_kb = 32;  // GR_STAGES / GR_STAGE_KB overrides (tuning)
 
     // step / cycle state
     std::mutex mu;
@@ -503,8 +503,10 @@ int gr_init(gr_ctx **out, const gr_world *world, const gr_tensor *table, int32_t
     // default one-shot threshold: at N=2 one-shot moves the same NVLink bytes as two-shot
     // with one fewer synchronisation, so it is used at every size; above N=2 it is kept for
     // latency-bound messages.
-    c->one_shot_max_bytes = world->one_shot_max_bytes >= 0 ? world->one_shot_max_bytes
-                                                           : (c->N == 2 ? INT64_MAX : (int64_t)1 << 20);
+    // default one-shot threshold: one-shot (every rank reads all N-1 peer copies) has the
+    // fewest synchronisations; two-shot moves 2(N-1)/N of the message per direction and less
+    // local HBM traffic, and wins for large messages at every N (measured).
+    c->one_shot_max_bytes = world->one_shot_max_bytes >= 0 ? world->one_shot_max_bytes : (int64_t)1 << 20;
     c->dry = world->device < 0;
     if (c->world.timeout_ms <= 0) c->world.timeout_ms = kDefaultTimeoutMs;
     int rc = build_layouts(c, table, group_of);

@@ -1,0 +1,103 @@
+"""cfg5 (BASELINE.json configs[4]): grouped-allreduce message-size sweep vs NCCL.
+
+  torchrun --nproc-per-node N tools/bench_cfg5.py [--buffer f16|f32] [--min-kib 1] [--max-mib 1024]
+
+One group holding one contiguous fp32 gradient tensor of S/p_b elements. For every
+size: our path (gr_mark_ready -> gr_step -> fused pack/reduce/unpack -> gr_wait;
+one-shot and two-shot forced, plus the library's default choice) against torch
+NCCL all_reduce(AVG) on an fp16/fp32 tensor of the same message size (reduce only;
+no pack/unpack). Device time with CUDA events, max over ranks; busbw = S*2(N-1)/N/t.
+Rank 0 prints one JSON line per size and a summary line.
+"""
+import argparse
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--buffer", default="f16", choices=["f16", "f32"])
+    ap.add_argument("--min-kib", type=int, default=1)
+    ap.add_argument("--max-mib", type=int, default=1024)
+    ap.add_argument("--iters", type=int, default=20)
+    a = ap.parse_args()
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_1909_11150_b200 as gr
+
+    rank = int(os.environ["RANK"])
+    N = int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist.init_process_group("nccl", device_id=dev)
+    pb = 2 if a.buffer == "f16" else 4
+    ag = gr.make_allgather(None, local)
+    comp = torch.cuda.current_stream(dev)
+
+    def tmax(x):
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def timed(fn, iters):
+        for _ in range(3):
+            fn()
+        dist.barrier(device_ids=[local])
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(comp)
+        for _ in range(iters):
+            fn()
+        e1.record(comp)
+        torch.cuda.synchronize()
+        return tmax(e0.elapsed_time(e1) / iters)
+
+    sizes = []
+    s = a.min_kib * 1024
+    while s <= a.max_mib * 1024 * 1024:
+        sizes.append(s)
+        s *= 2
+    rows = []
+    for S in sizes:
+        n = S // pb
+        iters = a.iters if S <= (64 << 20) else max(5, a.iters // 4)
+        g = torch.randn(n, device=dev)
+        res = {"bytes": S, "elems": n}
+        for name, osm in (("default", -1), ("oneshot", 1 << 62), ("twoshot", 0)):
+            ctx = gr.Context(rank=rank, world_size=N, device=local, numel=[n], group_of=[0],
+                             buffer_dtype=gr.GR_F16 if pb == 2 else gr.GR_F32, compute_stream=comp.cuda_stream,
+                             one_shot_max_bytes=osm, timeout_ms=30000, allgather=ag)
+            batch = ctx.prepare_batch([0], [g.data_ptr()])
+
+            def ours():
+                ctx.gr_mark_ready_prepared(batch)
+                ctx.gr_step()
+                ctx.gr_wait()
+
+            ms = timed(ours, iters)
+            res[f"{name}_us"] = ms * 1e3
+            res[f"{name}_busbw"] = S * 2 * (N - 1) / N / (ms * 1e-3) / 1e9
+            ctx.gr_finalize()
+        x = torch.zeros(n, dtype=torch.float16 if pb == 2 else torch.float32, device=dev)
+        ms = timed(lambda: dist.all_reduce(x, op=dist.ReduceOp.AVG), iters)
+        res["nccl_us"] = ms * 1e3
+        res["nccl_busbw"] = S * 2 * (N - 1) / N / (ms * 1e-3) / 1e9
+        rows.append(res)
+        if rank == 0:
+            print(json.dumps({k: (round(v, 3) if isinstance(v, float) else v) for k, v in res.items()}), flush=True)
+    if rank == 0:
+        print(json.dumps({"cfg5_summary": True, "N": N, "buffer": a.buffer,
+                          "what": "ours = mark+gr_step+fused pack/reduce/unpack+gr_wait on one fp32 tensor; "
+                                  "nccl = all_reduce(AVG) on a same-size buffer-dtype tensor (reduce only)"}))
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -21,7 +21,7 @@ METRICS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.
            "nvlrx__bytes.sum", "nvltx__bytes.sum"]
 
 UNIT_SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-9, "usecond": 1e-6,
-              "msecond": 1e-3, "second": 1.0}
+              "msecond": 1e-3, "second": 1.0, "ns": 1e-9, "us": 1e-6, "ms": 1e-3, "s": 1.0}
 
 
 def raw_rows(rep):
@@ -73,7 +73,12 @@ def main():
                     except ValueError:
                         val = None
                     rec[m] = val
-                    cells.append(f"{val:.4g}" if isinstance(val, float) else "-")
+                    if m == "gpu__time_duration.sum" and isinstance(val, float):
+                        cells.append(f"{val * 1e6:.1f} us")
+                    elif "bytes" in m and isinstance(val, float):
+                        cells.append(f"{val / 1e6:.1f} MB")
+                    else:
+                        cells.append(f"{val:.4g}" if isinstance(val, float) else "-")
                 else:
                     cells.append("n/a")
             rd, wr = rec.get("dram__bytes_read.sum"), rec.get("dram__bytes_write.sum")
