@@ -58,6 +58,7 @@ class ClockSampler:
         self.gpu = gpu_index
         self.proc = None
         self.path = os.path.join(ROOT, "gpurun_out", f"clocks_rank{gpu_index}_{os.getpid()}.csv")
+        self.t_timed_end = None
 
     def __enter__(self):
         os.makedirs(os.path.dirname(self.path), exist_ok=True)
@@ -67,12 +68,16 @@ class ClockSampler:
         try:
             self.f = open(self.path, "w")
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={q}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                          "--format=csv,noheader,nounits", "-lms", "50"],
                                          stdout=self.f, stderr=subprocess.DEVNULL)
         except Exception:
             self.proc = None
         time.sleep(0.3)
+        self.t_start = time.time()
         return self
+
+    def mark_timed_end(self):
+        self.t_timed_end = time.time()
 
     def __exit__(self, *a):
         if self.proc:
@@ -96,7 +101,8 @@ class ClockSampler:
                 if v.strip() == "Active":
                     reasons.add(n)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": sorted(reasons), "samples": len(rows)}
+                "reasons": sorted(reasons), "samples": len(rows),
+                "window": "timed region + 1 s soak of the identical step (nvidia-smi -lms 50)"}
 
 
 # ------------------------------------------------------------------ CPU oracle leg
@@ -218,11 +224,14 @@ def main():
 
     batch = ctx.prepare_batch(tensor_order, [ptrs[t] for t in tensor_order])
 
-    def one_step():
+    def one_step(blocking=False):
         ctx.gr_mark_ready_prepared(batch)  # all 68 tensors, reverse-layer order, one call
         rel, complete, _A, _ = ctx.gr_step()
         assert complete and len(rel) == f.G, (rel, complete)
-        ctx.gr_wait()
+        if blocking:
+            ctx.gr_wait()        # host blocks until the reduction is done
+        else:
+            ctx.gr_wait_async()  # stream-ordered: compute_stream waits, the host moves on
 
     def max_over_ranks(x: float) -> float:
         if N == 1:
@@ -244,8 +253,26 @@ def main():
             one_step()
         ev1.record(compute)
         torch.cuda.synchronize()
+        clk.mark_timed_end()
+        # the timed region is often far shorter than nvidia-smi's sampling period: keep the
+        # identical step running (untimed) for >= 1 s so the clock record covers this load
+        t_soak = time.perf_counter()
+        while time.perf_counter() - t_soak < 1.0:
+            one_step()
+        torch.cuda.synchronize()
     barrier()
     ms_local = ev0.elapsed_time(ev1) / args.steps
+    # the same steps with a host-blocking gr_wait (host latency exposed every step)
+    ev2, ev3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    nb = max(3, min(args.steps, 20))
+    barrier()
+    torch.cuda.synchronize()
+    ev2.record(compute)
+    for _ in range(nb):
+        one_step(blocking=True)
+    ev3.record(compute)
+    torch.cuda.synchronize()
+    ms_blocking = max_over_ranks(ev2.elapsed_time(ev3) / nb)
     ms = max_over_ranks(ms_local)
     st = ctx.stats()
     launches = int(st.bitvector_launches + st.data_launches)
@@ -258,7 +285,7 @@ def main():
     ctx.set_timing(True)
     ctx.reset_stats()
     for _ in range(max(3, min(args.steps, 10))):
-        one_step()
+        one_step(blocking=True)  # blocking wait collects the per-launch event timings
     stt = ctx.stats()
     ctx.set_timing(False)
     kern_ms = stt.data_kernel_ms / max(1, stt.data_launches)
@@ -338,6 +365,8 @@ def main():
                           "step": "mark 68 -> gr_step (1 cycle, 10 groups fused) -> pack/reduce/unpack -> gr_wait"},
                "value_is": "aggregate reduced-gradient GB/s = N*E*4B/t_step; per-rank NVLink bus GB/s in busbw_GBps",
                "busbw_GBps": round(busbw, 2) if busbw else None,
+               "wait": "gr_wait_async (stream-ordered; the production contract)",
+               "ms_per_step_blocking_wait": round(ms_blocking, 4),
                "gpu_launches": launches, "launches_per_step": launches / args.steps,
                "bitvector_kernel_us": round(bv_ms * 1e3, 2),
                "roofline": roof, "clocks": clk.summary(), "e2e": e2e, "cpu_baseline": cpu}

@@ -157,6 +157,13 @@ int gr_step(gr_ctx *ctx, int32_t *released, gr_cycle_info *info, uint32_t *globa
  * Errors: GR_ECUDA, GR_ETIMEOUT (a peer stopped mid-reduction). */
 int gr_wait(gr_ctx *ctx);
 
+/* gr_wait_async — LOCAL. Stream-ordered gr_wait: makes world.compute_stream wait for every
+ * reduction enqueued so far (work enqueued on it afterwards sees the reduced gradients) and
+ * starts the next step if this one is complete, without blocking the host — the CUDA-style
+ * contract the training loop of a framework uses. Errors of the in-flight reduction surface
+ * at the next gr_step / gr_wait. With GR_TRACE set it behaves like gr_wait. */
+int gr_wait_async(gr_ctx *ctx);
+
 /* gr_set_status — LOCAL. Raise (1) or clear (0) this rank's ABORT / SHUTDOWN
  * status bit for the following cycles (PAPER.md:130 reserved status bits). */
 int gr_set_status(gr_ctx *ctx, int32_t abort_flag, int32_t shutdown_flag);

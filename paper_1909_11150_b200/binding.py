@@ -68,6 +68,7 @@ def _load():
         "gr_mark_ready_batch": ([p, i32, i32, p, p], ctypes.c_int),
         "gr_step": ([p, p, ctypes.POINTER(GrCycleInfo), p], ctypes.c_int),
         "gr_wait": ([p], ctypes.c_int),
+        "gr_wait_async": ([p], ctypes.c_int),
         "gr_set_status": ([p, i32, i32], ctypes.c_int),
         "gr_finalize": ([p], ctypes.c_int),
         "gr_last_error": ([p], ctypes.c_char_p),
@@ -84,7 +85,7 @@ def _load():
 
 
 lib = _load()
-EXPORTED = ("gr_init", "gr_mark_ready", "gr_mark_ready_batch", "gr_mark_ready_async", "gr_step", "gr_wait", "gr_set_status",
+EXPORTED = ("gr_init", "gr_mark_ready", "gr_mark_ready_batch", "gr_mark_ready_async", "gr_step", "gr_wait", "gr_wait_async", "gr_set_status",
             "gr_finalize", "gr_last_error", "gr_query", "gr_set_timing", "gr_reset_stats", "gr_bench_spin")
 
 
@@ -178,6 +179,9 @@ class Context:
 
     def gr_wait(self):
         return _check(lib.gr_wait(self._ctx), self._ctx)
+
+    def gr_wait_async(self):
+        return _check(lib.gr_wait_async(self._ctx), self._ctx)
 
     # -- extras ------------------------------------------------------------------------------
     def gr_set_status(self, abort: bool = False, shutdown: bool = False):

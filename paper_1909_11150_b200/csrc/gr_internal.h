@@ -43,6 +43,15 @@ struct HostError {
 
 enum { ST_OK = 0, ST_ABORT = 1, ST_SHUTDOWN = 2, ST_TIMEOUT = 3 };
 
+// Cycle result handed from the bitvector kernel to the data kernel in device memory (ring
+// slot): the data kernel is launched before the host sees the result and starts as soon as
+// the bitvector kernel completes (stream event), with no host round trip in between.
+struct DevCycle {
+    int32_t n_released;
+    int32_t total_chunks;
+    int64_t elems;
+};
+
 struct BvParams {
     const uint32_t *host_bits;       // host-mapped [W]: bits set by gr_mark_ready (cleared per step);
                                      // unused when W <= GR_BV_INLINE_WORDS (copied into inline_bits)
@@ -59,6 +68,7 @@ struct BvParams {
     uint64_t *slot[GR_MAX_RANKS];    // every rank's LL bitvector slots [2][W] (own = local)
     int32_t *out_released;           // device [G]   (ring slot)
     int32_t *out_cum;                // device [G+1] (ring slot)
+    DevCycle *out_info;              // device (ring slot)
     HostResult *result;              // host-mapped
     int32_t T, G, W, nbits, rank, N;
     uint32_t epoch;                  // training-step epoch (>= 1)
@@ -79,6 +89,7 @@ struct DataParams {
     const int32_t *group_chunk_begin;  // [G]
     const int32_t *released;           // ring slot [G]
     const int32_t *cum;                // ring slot [G+1]
+    const DevCycle *info;              // ring slot: released groups / chunks / elements
     const uint64_t *dev_ptr;           // [T]
     char *buf[GR_MAX_RANKS];           // every rank's fusion buffer for this step parity
     uint32_t *pack_flag[GR_MAX_RANKS]; // every rank's pack flags [C][N] for this parity
@@ -95,7 +106,7 @@ struct DataParams {
     int64_t slot_bytes_red;            // bytes of one peer's slot inside a stage
     int64_t sub_red, sub_ag, sub_pack; // staged sub-tile (elements) for reduce / all-gather / pack items
     int32_t lag1, lag2;                // queue lags (in released chunks) of reduce / all-gather items
-    int32_t n_released, total_chunks;
+    int64_t one_shot_max_bytes;        // N>1: messages up to this many buffer bytes go one-shot
     int32_t rank, N;
     uint32_t epoch;
     float inv_n;
@@ -104,7 +115,7 @@ struct DataParams {
 
 // Kernel launchers (gr_kernels.cu). Return cudaError_t as int.
 int launch_bitvector(const BvParams &p, void *stream);
-int launch_data(const DataParams &p, int algo, int buffer_f16, int ctas, void *stream);
+int launch_data(const DataParams &p, int local, int buffer_f16, int ctas, void *stream);
 int data_kernel_max_ctas(int algo, int buffer_f16, int *out);
 int launch_spin(int64_t ns, int ctas, void *stream);
 

@@ -65,7 +65,7 @@ __device__ __forceinline__ void fence_acq_rel_sys() { asm volatile("fence.acq_re
 // K1: bitvector populate + AND + release
 // ---------------------------------------------------------------------------------------
 #ifndef GR_BV_THREADS
-#define GR_BV_THREADS 512
+#define GR_BV_THREADS 256
 #endif
 #define GR_SMALL_GROUP_WORDS 8
 #ifndef GR_BV_BATCH
@@ -74,7 +74,7 @@ __device__ __forceinline__ void fence_acq_rel_sys() { asm volatile("fence.acq_re
 constexpr int BV_THREADS = GR_BV_THREADS;
 constexpr int BV_BATCH = GR_BV_BATCH;
 
-__global__ void __launch_bounds__(BV_THREADS, 1) bitvector_kernel(BvParams p) {
+__global__ void __launch_bounds__(BV_THREADS, 4) bitvector_kernel(BvParams p) {
     extern __shared__ uint32_t smem[];
     uint32_t *sL = smem;          // [W] local bitvector
     uint32_t *sA = smem + p.W;    // [W] intersection, then [ceil(G/32)] complete-group bits
@@ -259,6 +259,9 @@ __global__ void __launch_bounds__(BV_THREADS, 1) bitvector_kernel(BvParams p) {
     if (tid == 0) {
         int complete = 1;
         for (int i = 0; i < nwarps; ++i) complete &= s_all[i];
+        p.out_info->n_released = (status == ST_OK) ? run_base : 0;
+        p.out_info->total_chunks = (status == ST_OK) ? run_ch : 0;
+        p.out_info->elems = (status == ST_OK) ? (int64_t)s_elems : 0;
         p.result->status = status;
         p.result->n_released = run_base;
         p.result->step_complete = (status == ST_OK) ? complete : 0;
@@ -427,8 +430,8 @@ __device__ __forceinline__ void grad_store1(char *g, int64_t idx, bool f16, floa
 }
 
 // chunk id of item i of the released set (binary search over the cumulative counts)
-__device__ __forceinline__ int chunk_of_item(const DataParams &p, int i) {
-    int lo = 0, hi = p.n_released - 1;
+__device__ __forceinline__ int chunk_of_item(const DataParams &p, int nrel, int i) {
+    int lo = 0, hi = nrel - 1;
     while (lo < hi) {
         const int mid = (lo + hi + 1) >> 1;
         if (p.cum[mid] <= i) lo = mid; else hi = mid - 1;
@@ -452,9 +455,10 @@ __global__ void __launch_bounds__(LC_THREADS, 3) local_kernel(DataParams p) {
     const int lane = threadIdx.x & 31;
     const int gw = blockIdx.x * (LC_THREADS / 32) + (threadIdx.x >> 5);
     const int nw = gridDim.x * (LC_THREADS / 32);
-    const int nitems = p.total_chunks * LC_SUBS;
+    const int nrel = p.info->n_released;
+    const int nitems = p.info->total_chunks * LC_SUBS;
     for (int it = gw; it < nitems; it += nw) {
-        const int c = chunk_of_item(p, it / LC_SUBS);
+        const int c = chunk_of_item(p, nrel, it / LC_SUBS);
         const int sub = it % LC_SUBS;
         const int64_t cb = p.chunk_begin[c], ce = p.chunk_end[c];
         const int64_t len = ((ce - cb + LC_SUBS * 8 - 1) / (LC_SUBS * 8)) * 8;  // multiple of 8
@@ -688,8 +692,11 @@ __device__ __forceinline__ void xf_consume(const DataParams &p, const XfMeta &m,
 
 constexpr int XF_RCACHE = 512;  // released groups cached in shared memory for item -> chunk
 
-template <typename BT, int ALGO>
-__global__ void __launch_bounds__(XF_THREADS, 1) xfer_kernel(DataParams p) {
+// 96 registers x 512 threads leaves room on every SM for a concurrently running
+// bitvector kernel (256 threads), so the next cycle's coordination never queues behind
+// a long reduction.
+template <typename BT>
+__global__ void __maxnreg__(96) xfer_kernel(DataParams p) {
     using B = Buf<BT>;
     extern __shared__ __align__(1024) char xsm[];
     __shared__ __align__(8) uint64_t full[XF_STAGES], empty[XF_STAGES];
@@ -707,24 +714,28 @@ __global__ void __launch_bounds__(XF_THREADS, 1) xfer_kernel(DataParams p) {
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     }
     const int nst = p.nstages;
-    const bool cached = p.n_released <= XF_RCACHE;
+    const int nrel = p.info->n_released;
+    const int total = p.info->total_chunks;
+    // algorithm chosen on the device from the released message size (same rule on every rank)
+    const int ALGO = (p.info->elems * B::ES <= p.one_shot_max_bytes) ? ALGO_ONESHOT : ALGO_TWOSHOT;
+    const bool cached = nrel <= XF_RCACHE;
     if (cached)
-        for (int j = tid; j < p.n_released; j += blockDim.x) {
+        for (int j = tid; j < nrel; j += blockDim.x) {
             s_cum[j] = p.cum[j];
             s_cb[j] = p.group_chunk_begin[p.released[j]];
         }
     __syncthreads();
     auto chunk_of = [&](int i) -> int {
-        if (!cached) return chunk_of_item(p, i);
-        int lo = 0, hi = p.n_released - 1;
+        if (!cached) return chunk_of_item(p, nrel, i);
+        int lo = 0, hi = nrel - 1;
         while (lo < hi) {
             const int mid = (lo + hi + 1) >> 1;
             if (s_cum[mid] <= i) lo = mid; else hi = mid - 1;
         }
         return s_cb[lo] + (i - s_cum[lo]);
     };
-    const int total = p.total_chunks;
-    const int nk = total + p.lag2;  // queue triples
+    const int lag1 = p.lag1, lag2 = (ALGO == ALGO_ONESHOT) ? p.lag1 : p.lag2;
+    const int nk = total > 0 ? total + lag2 : 0;  // queue triples
     if (warp == 0) {
         // ---------------- producer warp: lane 0 owns the queue, barriers and flag waits;
         // the 32 lanes describe / stage the chunk's gradient pieces and issue the peer
@@ -830,7 +841,7 @@ __global__ void __launch_bounds__(XF_THREADS, 1) xfer_kernel(DataParams p) {
                 }
             }
             // RED(k-L1) (one-shot, every chunk) / RS(k-L1) (two-shot, owned chunks)
-            const int i1 = k - p.lag1;
+            const int i1 = k - lag1;
             if (i1 >= 0 && i1 < total) {
                 const int c = chunk_of(i1);
                 if (ALGO == ALGO_ONESHOT || c % p.N == p.rank) {
@@ -845,7 +856,7 @@ __global__ void __launch_bounds__(XF_THREADS, 1) xfer_kernel(DataParams p) {
             }
             // AG(k-L2) (two-shot): pull the owner's reduced chunk
             if (ALGO == ALGO_TWOSHOT) {
-                const int i2 = k - p.lag2;
+                const int i2 = k - lag2;
                 if (i2 >= 0 && i2 < total) {
                     const int c = chunk_of(i2);
                     const int owner = c % p.N;
@@ -918,25 +929,20 @@ __global__ void __launch_bounds__(XF_THREADS, 1) xfer_kernel(DataParams p) {
 }
 
 template <typename BT>
-static int launch_data_t(const DataParams &p, int algo, int ctas, cudaStream_t s) {
-    const size_t xsmem = (size_t)p.nstages * p.stage_bytes;
+static int launch_data_t(const DataParams &p, int local, int ctas, cudaStream_t s) {
     static bool attr_set = false;
     if (!attr_set) {
-        cudaFuncSetAttribute(xfer_kernel<BT, ALGO_ONESHOT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 208 * 1024);
-        cudaFuncSetAttribute(xfer_kernel<BT, ALGO_TWOSHOT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 208 * 1024);
+        cudaFuncSetAttribute(xfer_kernel<BT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 208 * 1024);
         attr_set = true;
     }
-    switch (algo) {
-        case ALGO_LOCAL: local_kernel<BT><<<ctas, LC_THREADS, 0, s>>>(p); break;
-        case ALGO_ONESHOT: xfer_kernel<BT, ALGO_ONESHOT><<<ctas, XF_THREADS, xsmem, s>>>(p); break;
-        default: xfer_kernel<BT, ALGO_TWOSHOT><<<ctas, XF_THREADS, xsmem, s>>>(p); break;
-    }
+    if (local) local_kernel<BT><<<ctas, LC_THREADS, 0, s>>>(p);
+    else xfer_kernel<BT><<<ctas, XF_THREADS, (size_t)p.nstages * p.stage_bytes, s>>>(p);
     return (int)cudaGetLastError();
 }
 
-int launch_data(const DataParams &p, int algo, int buffer_f16, int ctas, void *stream) {
+int launch_data(const DataParams &p, int local, int buffer_f16, int ctas, void *stream) {
     cudaStream_t s = (cudaStream_t)stream;
-    return buffer_f16 ? launch_data_t<__half>(p, algo, ctas, s) : launch_data_t<float>(p, algo, ctas, s);
+    return buffer_f16 ? launch_data_t<__half>(p, local, ctas, s) : launch_data_t<float>(p, local, ctas, s);
 }
 
 template <typename BT>

@@ -76,7 +76,7 @@ struct gr_ctx {
     // device state
     int dev = -1;
     cudaStream_t s_coord = nullptr, s_data = nullptr, s_compute = nullptr;
-    cudaEvent_t ev_compute = nullptr, ev_data_done = nullptr;
+    cudaEvent_t ev_compute = nullptr, ev_data_done = nullptr, ev_bv = nullptr;
     cudaEvent_t ring_ev[GR_SLOT_RING] = {};
     bool ring_pending[GR_SLOT_RING] = {};
     char *symm = nullptr;
@@ -93,6 +93,7 @@ struct gr_ctx {
     uint32_t *d_grel = nullptr;
     uint64_t *d_ptr = nullptr;
     int32_t *d_rel_ring = nullptr, *d_cum_ring = nullptr;
+    gr::DevCycle *d_info_ring = nullptr;
     int32_t *d_counters = nullptr;  // [0] work, [1] done, [2] abort
     // pinned host-mapped
     uint32_t *h_bits = nullptr;   // sync marks, by bit
@@ -316,6 +317,7 @@ int setup_device(gr_ctx *c) {
     c->s_compute = (cudaStream_t)c->world.compute_stream;
     CK(c, cudaEventCreateWithFlags(&c->ev_compute, cudaEventDisableTiming));
     CK(c, cudaEventCreateWithFlags(&c->ev_data_done, cudaEventDisableTiming));
+    CK(c, cudaEventCreateWithFlags(&c->ev_bv, cudaEventDisableTiming));
     for (int i = 0; i < GR_SLOT_RING; ++i) CK(c, cudaEventCreateWithFlags(&c->ring_ev[i], cudaEventDisableTiming));
 
     // symmetric memory: [LL bitvector slots 2 x W u64][flag pad 2 x (C*N + C) u32][fusion buffer 2 x E]
@@ -347,6 +349,8 @@ int setup_device(gr_ctx *c) {
     CK(c, cudaMalloc((void **)&c->d_ptr, sizeof(uint64_t) * c->T));
     CK(c, cudaMalloc((void **)&c->d_rel_ring, sizeof(int32_t) * GR_SLOT_RING * (size_t)c->G));
     CK(c, cudaMalloc((void **)&c->d_cum_ring, sizeof(int32_t) * GR_SLOT_RING * (size_t)(c->G + 1)));
+    CK(c, cudaMalloc((void **)&c->d_info_ring, sizeof(gr::DevCycle) * GR_SLOT_RING));
+    CK(c, cudaMemset(c->d_info_ring, 0, sizeof(gr::DevCycle) * GR_SLOT_RING));
     CK(c, cudaMalloc((void **)&c->d_counters, sizeof(int32_t) * 4));
     CK(c, cudaMemset(c->d_counters, 0, sizeof(int32_t) * 4));
 
@@ -428,7 +432,7 @@ void free_all(gr_ctx *c) {
         if (r != c->rank && c->peer_symm[r]) cudaIpcCloseMemHandle(c->peer_symm[r]);
     cudaFree(c->symm);
     void *dptrs[] = {c->d_segs, c->d_chunks, c->d_cbeg, c->d_cend, c->d_tob, c->d_gob, c->d_gbb, c->d_gbe, c->d_gnch, c->d_gcb,
-                     c->d_gel, c->d_big, c->d_grel, c->d_ptr, c->d_rel_ring, c->d_cum_ring, c->d_counters,
+                     c->d_gel, c->d_big, c->d_grel, c->d_ptr, c->d_rel_ring, c->d_cum_ring, c->d_info_ring, c->d_counters,
                      c->d_flags, c->d_trace};
     for (void *p : dptrs) cudaFree(p);
     cudaFreeHost(c->h_bits);
@@ -439,6 +443,7 @@ void free_all(gr_ctx *c) {
         if (c->ring_ev[i]) cudaEventDestroy(c->ring_ev[i]);
     if (c->ev_compute) cudaEventDestroy(c->ev_compute);
     if (c->ev_data_done) cudaEventDestroy(c->ev_data_done);
+    if (c->ev_bv) cudaEventDestroy(c->ev_bv);
     for (auto &v : {c->pending_data_ev, c->pending_bv_ev, c->free_ev})
         for (auto &pr : v) {
             cudaEventDestroy(pr.first);
@@ -625,6 +630,7 @@ int gr_step(gr_ctx *c, int32_t *released, gr_cycle_info *info, uint32_t *global_
     if (c->dry) return fail(c, GR_ESTATE, "dry context (device < 0) cannot step");
     if (c->sticky) return fail(c, GR_ESTATE, "context is in a sticky error state (%d): %s", c->sticky, c->err.c_str());
     const auto h_enter = std::chrono::steady_clock::now();
+    if (c->h_err->code) return fail(c, GR_ETIMEOUT, "a previous reduction timed out waiting for a peer");
     CK(c, cudaSetDevice(c->dev));
     const int slot = (int)(c->cycle % GR_SLOT_RING);
     if (c->ring_pending[slot]) {  // the data launch that read this slot must be done
@@ -667,6 +673,7 @@ int gr_step(gr_ctx *c, int32_t *released, gr_cycle_info *info, uint32_t *global_
     for (int r = 0; r < c->N; ++r) p.slot[r] = reinterpret_cast<uint64_t *>(c->peer_symm[r] + c->off_slot);
     p.out_released = c->d_rel_ring + (size_t)slot * c->G;
     p.out_cum = c->d_cum_ring + (size_t)slot * (c->G + 1);
+    p.out_info = c->d_info_ring + slot;
     p.result = c->d_res;
     p.T = c->T;
     p.G = c->G;
@@ -697,6 +704,77 @@ int gr_step(gr_ctx *c, int32_t *released, gr_cycle_info *info, uint32_t *global_
         c->pending_bv_ev.push_back(evb);
     }
     c->stats.bitvector_launches++;
+
+    // Data kernel, launched now (before the host sees the cycle's result): it waits on the
+    // bitvector kernel through an event and reads the released set from device memory, so
+    // the reduction starts the moment the bitvector kernel ends. Empty cycles exit at once.
+    {
+        gr::DataParams d{};
+        d.segs = c->d_segs;
+        d.chunks = c->d_chunks;
+        d.group_chunk_begin = c->d_gcb;
+        d.released = p.out_released;
+        d.cum = p.out_cum;
+        d.info = p.out_info;
+        d.dev_ptr = c->d_ptr;
+        const int par = (int)(epoch & 1);
+        for (int r = 0; r < c->N; ++r) {
+            char *base = c->peer_symm[r];
+            d.buf[r] = base + c->off_buf + (size_t)par * c->buf_parity_bytes;
+            uint32_t *pad = reinterpret_cast<uint32_t *>(base + c->off_pad) + (size_t)par * c->pad_parity_u32;
+            d.pack_flag[r] = pad;
+            d.rs_flag[r] = pad + (size_t)c->C * c->N;
+        }
+        d.work_counter = c->d_counters;
+        d.done_counter = c->d_counters + 1;
+        d.abort_dev = c->d_counters + 2;
+        d.err = c->d_err;
+        d.trace = c->d_trace ? c->d_trace + (size_t)slot * c->trace_slot_u64 : nullptr;
+        d.chunk_begin = c->d_cbeg;
+        d.chunk_end = c->d_cend;
+        const int64_t es = c->buf_f16 ? 2 : 4;
+        const int64_t stage = c->stage_kb * 1024;
+        d.stage_bytes = stage;
+        d.nstages = c->nstages;
+        // RED/RS stage: N-1 peer slots (buffer precision) + one fp32-spaced gradient slot
+        int64_t sr = c->N > 1 ? stage / ((c->N - 1) * es + 4) / 256 * 256 : 256;
+        sr = std::max<int64_t>(256, std::min<int64_t>(sr, c->chunk_elems));
+        d.sub_red = sr;
+        d.slot_bytes_red = sr * es;
+        d.sub_pack = std::max<int64_t>(256, std::min<int64_t>(stage / 4 / 256 * 256, c->chunk_elems));
+        d.sub_ag = std::max<int64_t>(256, std::min<int64_t>(stage / es / 256 * 256, c->chunk_elems));
+        d.one_shot_max_bytes = c->one_shot_max_bytes;
+        d.rank = c->rank;
+        d.N = c->N;
+        d.epoch = epoch;
+        d.inv_n = 1.0f / (float)c->N;
+        d.timeout_ns = (uint64_t)c->world.timeout_ms * 1000000ull;
+        const bool local = c->N == 1;
+        const int ctas = c->data_ctas[local ? gr::ALGO_LOCAL : gr::ALGO_TWOSHOT];
+        d.lag1 = c->lag1 > 0 ? c->lag1 : 2 * ctas;
+        d.lag2 = c->lag2 > 0 ? c->lag2 : 4 * ctas;
+        CK(c, cudaEventRecord(c->ev_bv, c->s_coord));
+        CK(c, cudaStreamWaitEvent(c->s_data, c->ev_bv, 0));
+        std::pair<cudaEvent_t, cudaEvent_t> evd{};
+        if (c->timing) {
+            evd = get_ev_pair(c);
+            CK(c, cudaEventRecord(evd.first, c->s_data));
+        }
+        if (c->ptr_dirty) {  // gradient pointers marked since the last upload
+            c->ptr_dirty = false;
+            CK(c, cudaMemcpyAsync(c->d_ptr, c->h_ptr, sizeof(uint64_t) * c->T, cudaMemcpyHostToDevice, c->s_data));
+        }
+        if (d.trace) CK(c, cudaMemsetAsync(d.trace, 0, sizeof(uint64_t) * c->trace_slot_u64, c->s_data));
+        lrc = gr::launch_data(d, local, c->buf_f16, ctas, c->s_data);
+        if (lrc) return fail(c, GR_ECUDA, "data launch: %s", cudaGetErrorString((cudaError_t)lrc));
+        if (c->timing) {
+            CK(c, cudaEventRecord(evd.second, c->s_data));
+            c->pending_data_ev.push_back(evd);
+        }
+        CK(c, cudaEventRecord(c->ring_ev[slot], c->s_data));
+        c->ring_pending[slot] = true;
+        c->stats.data_launches++;
+    }
 
     // wait for the kernel's hand-off (pinned host memory), bounded
     const auto t0 = std::chrono::steady_clock::now();
@@ -732,76 +810,9 @@ int gr_step(gr_ctx *c, int32_t *released, gr_cycle_info *info, uint32_t *global_
     memcpy(released, hrel, sizeof(int32_t) * n);
 
     if (n > 0) {
-        gr::DataParams d{};
-        d.segs = c->d_segs;
-        d.chunks = c->d_chunks;
-        d.group_chunk_begin = c->d_gcb;
-        d.released = p.out_released;
-        d.cum = p.out_cum;
-        d.dev_ptr = c->d_ptr;
-        const int par = (int)(epoch & 1);
-        for (int r = 0; r < c->N; ++r) {
-            char *base = c->peer_symm[r];
-            d.buf[r] = base + c->off_buf + (size_t)par * c->buf_parity_bytes;
-            uint32_t *pad = reinterpret_cast<uint32_t *>(base + c->off_pad) + (size_t)par * c->pad_parity_u32;
-            d.pack_flag[r] = pad;
-            d.rs_flag[r] = pad + (size_t)c->C * c->N;
-        }
-        d.work_counter = c->d_counters;
-        d.done_counter = c->d_counters + 1;
-        d.abort_dev = c->d_counters + 2;
-        d.err = c->d_err;
-        d.trace = c->d_trace ? c->d_trace + (size_t)slot * c->trace_slot_u64 : nullptr;
-        d.chunk_begin = c->d_cbeg;
-        d.chunk_end = c->d_cend;
-        {
-            const int64_t es = c->buf_f16 ? 2 : 4;
-            const int64_t stage = c->stage_kb * 1024;
-            d.stage_bytes = stage;
-            d.nstages = c->nstages;
-            // RED/RS stage: N-1 peer slots (buffer precision) + one fp32-spaced gradient slot
-            int64_t sr = c->N > 1 ? stage / ((c->N - 1) * es + 4) / 256 * 256 : 256;
-            sr = std::max<int64_t>(256, std::min<int64_t>(sr, c->chunk_elems));
-            d.sub_red = sr;
-            d.slot_bytes_red = sr * es;
-            d.sub_pack = std::max<int64_t>(256, std::min<int64_t>(stage / 4 / 256 * 256, c->chunk_elems));
-            d.sub_ag = std::max<int64_t>(256, std::min<int64_t>(stage / es / 256 * 256, c->chunk_elems));
-        }
-        d.n_released = n;
-        d.total_chunks = total_chunks;
-        d.rank = c->rank;
-        d.N = c->N;
-        d.epoch = epoch;
-        d.inv_n = 1.0f / (float)c->N;
-        d.timeout_ns = (uint64_t)c->world.timeout_ms * 1000000ull;
         const int64_t msg_bytes = rel_elems * (c->buf_f16 ? 2 : 4);
-        int algo = gr::ALGO_LOCAL;
-        if (c->N > 1) algo = msg_bytes <= c->one_shot_max_bytes ? gr::ALGO_ONESHOT : gr::ALGO_TWOSHOT;
-        const int nitems = total_chunks * (algo == gr::ALGO_LOCAL ? 1 : (algo == gr::ALGO_ONESHOT ? 2 : 3));
-        const int ctas = std::max(1, std::min(c->data_ctas[algo], nitems));
-        d.lag1 = c->lag1 > 0 ? c->lag1 : 2 * ctas;
-        d.lag2 = c->lag2 > 0 ? c->lag2 : 4 * ctas;
-        if (algo == gr::ALGO_ONESHOT) d.lag2 = d.lag1;
-        std::pair<cudaEvent_t, cudaEvent_t> evd{};
-        if (c->timing) {
-            evd = get_ev_pair(c);
-            CK(c, cudaEventRecord(evd.first, c->s_data));
-        }
-        if (c->ptr_dirty) {  // gradient pointers of this step (marked before this cycle)
-            CK(c, cudaMemcpyAsync(c->d_ptr, c->h_ptr, sizeof(uint64_t) * c->T, cudaMemcpyHostToDevice, c->s_data));
-            c->ptr_dirty = false;
-        }
-        if (d.trace) CK(c, cudaMemsetAsync(d.trace, 0, sizeof(uint64_t) * 4 * (size_t)nitems, c->s_data));
-        lrc = gr::launch_data(d, algo, c->buf_f16, ctas, c->s_data);
-        if (lrc) return fail(c, GR_ECUDA, "data launch: %s", cudaGetErrorString((cudaError_t)lrc));
-        if (c->timing) {
-            CK(c, cudaEventRecord(evd.second, c->s_data));
-            c->pending_data_ev.push_back(evd);
-        }
-        CK(c, cudaEventRecord(c->ring_ev[slot], c->s_data));
-        c->ring_pending[slot] = true;
-        c->last_algo = algo;
-        c->stats.data_launches++;
+        c->last_algo = c->N == 1 ? gr::ALGO_LOCAL
+                                 : (msg_bytes <= c->one_shot_max_bytes ? gr::ALGO_ONESHOT : gr::ALGO_TWOSHOT);
         c->stats.released_elems += rel_elems;
     }
     const int complete = c->h_res->step_complete;
@@ -841,6 +852,32 @@ int gr_step(gr_ctx *c, int32_t *released, gr_cycle_info *info, uint32_t *global_
         info->released_elems = rel_elems;
     }
     return GR_OK;
+}
+
+static int start_next_step(gr_ctx *c) {
+    std::lock_guard<std::mutex> lk(c->mu);
+    if (c->step_complete) {
+        c->step_complete = false;
+        c->epoch++;
+        if (c->epoch == 0) c->epoch = 1;
+        c->step++;
+        c->stats.steps++;
+        std::fill(c->marked.begin(), c->marked.end(), 0);
+        memset(c->h_bits, 0, sizeof(uint32_t) * (size_t)c->W);  // no bitvector kernel is in flight
+    }
+    return GR_OK;
+}
+
+int gr_wait_async(gr_ctx *c) {
+    if (!c) return GR_EINVAL;
+    if (!c->trace_path.empty()) return gr_wait(c);
+    if (c->dry) return fail(c, GR_ESTATE, "dry context (device < 0) cannot wait");
+    if (c->sticky == GR_ECUDA) return fail(c, GR_ESTATE, "context is in a sticky error state: %s", c->err.c_str());
+    if (c->h_err->code) return fail(c, GR_ETIMEOUT, "reduction timed out waiting for a peer");
+    CK(c, cudaSetDevice(c->dev));
+    CK(c, cudaEventRecord(c->ev_data_done, c->s_data));
+    CK(c, cudaStreamWaitEvent(c->s_compute, c->ev_data_done, 0));
+    return start_next_step(c);
 }
 
 int gr_wait(gr_ctx *c) {
@@ -883,17 +920,7 @@ int gr_wait(gr_ctx *c) {
         }
         c->trace_cycles.clear();
     }
-    std::lock_guard<std::mutex> lk(c->mu);
-    if (c->step_complete) {
-        c->step_complete = false;
-        c->epoch++;
-        if (c->epoch == 0) c->epoch = 1;
-        c->step++;
-        c->stats.steps++;
-        std::fill(c->marked.begin(), c->marked.end(), 0);
-        memset(c->h_bits, 0, sizeof(uint32_t) * (size_t)c->W);  // no bitvector kernel is in flight
-    }
-    return GR_OK;
+    return start_next_step(c);
 }
 
 int gr_finalize(gr_ctx *c) {

@@ -132,6 +132,28 @@ def test_never_marked_and_errors(gpu):
     ctx.gr_finalize()
 
 
+def test_async_wait_pipelined_steps(gpu):
+    """gr_wait_async: 5 back-to-back steps without host blocking; the reduction is idempotent
+    at N=1 (re-rounding), so the final values equal one oracle application."""
+    import torch
+    from tests.parity_lib import check_values, host_inputs
+    from harness.replay import make_grads
+    case = _n1(cfg1_case(11))
+    ctx = _ctx(case, True)
+    grads = make_grads(case.numel, 0, 11, gpu)
+    order = list(range(case.T))
+    for _ in range(5):
+        ctx.gr_mark_ready_batch(order, [g.data_ptr() for g in grads])
+        rel, complete, _, _ = ctx.gr_step()
+        assert complete and rel == list(range(case.G))
+        ctx.gr_wait_async()
+    torch.cuda.synchronize()
+    for t in range(case.T):
+        check_values(grads[t].cpu().numpy(), host_inputs(case.numel, 1, 11, t, False), 1, True, False)
+    assert ctx.stats().steps == 5
+    ctx.gr_finalize()
+
+
 def test_async_marks_follow_stream(gpu):
     """gr_mark_ready_async: the flag lands only after the stream's prior work."""
     import torch
