@@ -262,6 +262,7 @@ def main():
         torch.cuda.synchronize()
     barrier()
     ms_local = ev0.elapsed_time(ev1) / args.steps
+    ctx_nvls = "%s (%s)" % ctx.nvls() if N > 1 else None
     # the same steps with a host-blocking gr_wait (host latency exposed every step)
     ev2, ev3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     nb = max(3, min(args.steps, 20))
@@ -308,7 +309,7 @@ def main():
         alg_bytes = int(2 * (N - 1) / N * S)  # bytes that must cross NVLink per direction per rank
         roof = {"bound": "nvlink", "achieved": round(alg_bytes / (kern_ms * 1e-3) / 1e9, 1), "peak": 770.0,
                 "unit": "GB/s", "peak_source": "B200_PROFILING.md measured peer copy per direction (900 nominal)",
-                "kernel": f"xfer_kernel<{'half' if buf16 else 'float'},{'TWOSHOT' if algo == 3 else 'ONESHOT'}>",
+                "kernel": f"xfer_kernel<{'half' if buf16 else 'float'}>:{ {2: 'ONESHOT', 3: 'TWOSHOT', 4: 'NVLS'}.get(algo) }",
                 "algorithmic_bytes_per_launch": alg_bytes, "kernel_ms": round(kern_ms, 4)}
     roof["frac"] = round(roof["achieved"] / roof["peak"], 4)
     roof["traffic"] = None
@@ -360,8 +361,9 @@ def main():
                "data": "synthetic (counter-based seeded fp32 gradients; fcn220m shapes, SURVEY.md App. A)",
                "config": {"workload": "fcn220m_cfg2_pack_scale_unpack" if N == 1 else "fcn220m_cfg3_bitvector_grouping",
                           "tensors": f.T, "groups": f.G, "elements": E, "buffer": args.buffer,
-                          "message_bytes": S, "algo": {1: "local", 2: "one-shot", 3: "two-shot"}.get(algo),
+                          "message_bytes": S, "algo": {1: "local", 2: "one-shot", 3: "two-shot", 4: "nvls"}.get(algo),
                           "l2": "inputs 900 MB/rank > 126 MB L2 (no flush needed)",
+                          "nvls": ctx_nvls,
                           "step": "mark 68 -> gr_step (1 cycle, 10 groups fused) -> pack/reduce/unpack -> gr_wait"},
                "value_is": "aggregate reduced-gradient GB/s = N*E*4B/t_step; per-rank NVLink bus GB/s in busbw_GBps",
                "busbw_GBps": round(busbw, 2) if busbw else None,

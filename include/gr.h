@@ -182,13 +182,19 @@ const char *gr_last_error(gr_ctx *ctx);
  *   GR_Q_BUF_OFFSET   int64[T]       element offset of each tensor in the fusion buffer
  *   GR_Q_NCHUNKS      int32          chunks of the static layout
  *   GR_Q_STATS        gr_stats       counters (launches, cycles, bytes)
- *   GR_Q_LAST_ALGO    int32          algorithm of the last data launch (gr_algo) */
+ *   GR_Q_LAST_ALGO    int32          algorithm of the last data launch (gr_algo)
+ *   GR_Q_NVLS         int32          1 if the NVLS multicast path is enabled
+ *   GR_Q_NVLS_WHY     char[bytes]    why it is (not) enabled, NUL-terminated */
 typedef enum {
     GR_Q_WORDS = 0, GR_Q_BIT_OF = 1, GR_Q_BUF_OFFSET = 2, GR_Q_NCHUNKS = 3,
-    GR_Q_STATS = 4, GR_Q_LAST_ALGO = 5
+    GR_Q_STATS = 4, GR_Q_LAST_ALGO = 5, GR_Q_NVLS = 6, GR_Q_NVLS_WHY = 7
 } gr_query_kind;
 
-typedef enum { GR_ALGO_NONE = 0, GR_ALGO_LOCAL = 1, GR_ALGO_ONESHOT = 2, GR_ALGO_TWOSHOT = 3 } gr_algo;
+/* GR_ALGO_NVLS: the reduce-scatter runs inside the NVSwitch (multimem.ld_reduce through a
+ * multicast mapping, fp32 accumulation) and the result is broadcast with multimem.st; on by
+ * default from N = 8 when every GPU supports multicast (environment GR_NVLS=0/1 overrides). */
+typedef enum { GR_ALGO_NONE = 0, GR_ALGO_LOCAL = 1, GR_ALGO_ONESHOT = 2, GR_ALGO_TWOSHOT = 3,
+               GR_ALGO_NVLS = 4 } gr_algo;
 
 typedef struct {
     int64_t cycles;             /* gr_step calls */

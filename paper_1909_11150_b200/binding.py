@@ -18,8 +18,8 @@ GR_OK, GR_EINVAL, GR_ESTATE, GR_EMISMATCH, GR_ECUDA, GR_ETIMEOUT, GR_EABORT, GR_
 STATUS_NAMES = {0: "GR_OK", -1: "GR_EINVAL", -2: "GR_ESTATE", -3: "GR_EMISMATCH", -4: "GR_ECUDA",
                 -5: "GR_ETIMEOUT", -6: "GR_EABORT", -7: "GR_ESHUTDOWN", -8: "GR_ENOMEM"}
 GR_F32, GR_F16 = 0, 1
-GR_Q_WORDS, GR_Q_BIT_OF, GR_Q_BUF_OFFSET, GR_Q_NCHUNKS, GR_Q_STATS, GR_Q_LAST_ALGO = range(6)
-GR_ALGO_NONE, GR_ALGO_LOCAL, GR_ALGO_ONESHOT, GR_ALGO_TWOSHOT = range(4)
+GR_Q_WORDS, GR_Q_BIT_OF, GR_Q_BUF_OFFSET, GR_Q_NCHUNKS, GR_Q_STATS, GR_Q_LAST_ALGO, GR_Q_NVLS, GR_Q_NVLS_WHY = range(8)
+GR_ALGO_NONE, GR_ALGO_LOCAL, GR_ALGO_ONESHOT, GR_ALGO_TWOSHOT, GR_ALGO_NVLS = range(5)
 
 ALLGATHER_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p)
 
@@ -201,6 +201,12 @@ class Context:
         a = (ctypes.c_int64 * self.T)()
         _check(lib.gr_query(self._ctx, GR_Q_BUF_OFFSET, a, 8 * self.T), self._ctx)
         return list(a)
+
+    def nvls(self):
+        """(enabled, reason) of the NVLS multicast path."""
+        buf = ctypes.create_string_buffer(256)
+        _check(lib.gr_query(self._ctx, GR_Q_NVLS_WHY, buf, 256), self._ctx)
+        return self.query_int(GR_Q_NVLS) == 1, buf.value.decode()
 
     def stats(self) -> GrStats:
         s = GrStats()

@@ -53,18 +53,18 @@ struct DevCycle {
 };
 
 struct BvParams {
-    const uint32_t *host_bits;       // host-mapped [W]: bits set by gr_mark_ready (cleared per step);
-                                     // unused when W <= GR_BV_INLINE_WORDS (copied into inline_bits)
+    const uint32_t *host_bits;       // device copy [W] of the host mark bits (DMA'd before the launch);
+                                     // unused when W <= GR_BV_INLINE_WORDS (passed in inline_bits)
     const uint32_t *dev_flags;       // device [W*32]: step epoch written by gr_mark_ready_async
-    const int32_t *tensor_of_bit;    // device [nbits]
-    const int32_t *group_of_bit;     // device [nbits]
+    uint32_t *rel_words;             // device [W]: tensor bits released so far in this step
+    int32_t new_step;                // 1 on the first cycle of a step (rel_words restart at 0)
+    int32_t check_async;             // 1 if gr_mark_ready_async was used in this step
     const int32_t *group_bit_begin;  // device [G]
     const int32_t *group_bit_end;    // device [G]
     const int32_t *group_nchunks;    // device [G]
     const int64_t *group_elems;      // device [G]
     const int32_t *big_groups;       // device [n_big]: groups spanning > 8 bitvector words
     int32_t n_big;
-    uint32_t *group_rel_epoch;       // device [G]: epoch in which the group was released
     uint64_t *slot[GR_MAX_RANKS];    // every rank's LL bitvector slots [2][W] (own = local)
     int32_t *out_released;           // device [G]   (ring slot)
     int32_t *out_cum;                // device [G+1] (ring slot)
@@ -81,7 +81,7 @@ struct BvParams {
     uint32_t inline_bits[GR_BV_INLINE_WORDS];  // snapshot of host_bits passed with the launch
 };
 
-enum Algo { ALGO_LOCAL = 1, ALGO_ONESHOT = 2, ALGO_TWOSHOT = 3 };
+enum Algo { ALGO_LOCAL = 1, ALGO_ONESHOT = 2, ALGO_TWOSHOT = 3, ALGO_NVLS = 4 };
 
 struct DataParams {
     const Seg *segs;
@@ -92,6 +92,8 @@ struct DataParams {
     const DevCycle *info;              // ring slot: released groups / chunks / elements
     const uint64_t *dev_ptr;           // [T]
     char *buf[GR_MAX_RANKS];           // every rank's fusion buffer for this step parity
+    char *nvls_uc;                     // NVLS: this rank's copy of the multicast buffer (parity), or null
+    char *nvls_mc;                     // NVLS: the multicast view of it (multimem.*), or null
     uint32_t *pack_flag[GR_MAX_RANKS]; // every rank's pack flags [C][N] for this parity
     uint32_t *rs_flag[GR_MAX_RANKS];   // every rank's reduce-scatter flags [C] for this parity
     int32_t *work_counter;             // device, reset by the last CTA

@@ -74,50 +74,49 @@ __device__ __forceinline__ void fence_acq_rel_sys() { asm volatile("fence.acq_re
 constexpr int BV_THREADS = GR_BV_THREADS;
 constexpr int BV_BATCH = GR_BV_BATCH;
 
+// Shared memory: sL[W] local bitvector, sA[W] intersection, sR[W] released-tensor bits of
+// this step, sC[Gw] complete-group bits (Gw = ceil(G/32)).
 __global__ void __launch_bounds__(BV_THREADS, 4) bitvector_kernel(BvParams p) {
     extern __shared__ uint32_t smem[];
-    uint32_t *sL = smem;          // [W] local bitvector
-    uint32_t *sA = smem + p.W;    // [W] intersection, then [ceil(G/32)] complete-group bits
+    const int W = p.W, G = p.G, Gw = (p.G + 31) / 32;
+    uint32_t *sL = smem, *sA = smem + W, *sR = smem + 2 * W, *sC = smem + 3 * W;
     __shared__ int s_timeout;
-    __shared__ int s_wcnt[32], s_wch[32];
-    __shared__ int s_tot_cnt, s_tot_ch;
+    __shared__ int s_scan[BV_THREADS / 32][2];
     __shared__ unsigned long long s_elems;
-    __shared__ int s_all[32];
+    __shared__ int s_all[BV_THREADS / 32];
+    __shared__ int s_tot[2];
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
     const uint64_t t_start = globaltimer();
     if (tid == 0) { s_timeout = 0; s_elems = 0ull; }
+    // released bits of this step (a new step starts from none)
+    for (int w = tid; w < W; w += blockDim.x) sR[w] = p.new_step ? 0u : p.rel_words[w];
+    for (int i = tid; i < Gw; i += blockDim.x) sC[i] = 0u;
+    __syncthreads();
 
     // ---- step 1: populate from pending requests, publish ----
-    // ready(b) = host-marked bit (gr_mark_ready) OR device flag == epoch (gr_mark_ready_async);
-    // pending(b) = ready(b) AND its group not yet released in this step (reading R4).
-    uint64_t *my_slot = p.slot[p.rank] + (size_t)p.parity * p.W;
-    for (int w0 = warp; w0 < p.W; w0 += nwarps * BV_BATCH) {
+    // ready = host marks (gr_mark_ready, bits) | async marks (device flag == epoch, ballot);
+    // pending = ready & ~released (reading R4: a ready tensor stays pending until its group goes)
+    uint64_t *my_slot = p.slot[p.rank] + (size_t)p.parity * W;
+    for (int w0 = warp; w0 < W; w0 += nwarps * BV_BATCH) {
         uint32_t f[BV_BATCH], hb[BV_BATCH];
-        int gob[BV_BATCH];
 #pragma unroll
         for (int k = 0; k < BV_BATCH; ++k) {  // issue the independent loads first
             const int w = w0 + k * nwarps;
             const int b = w * 32 + lane;
-            const bool valid = w < p.W && b >= GR_STATUS_BITS && b < p.nbits;
-            f[k] = valid ? ld_relaxed_sys32(p.dev_flags + b) : 0u;
-            hb[k] = (w < p.W) ? (p.use_inline ? p.inline_bits[w] : ld_relaxed_sys32(p.host_bits + w)) : 0u;
-            gob[k] = valid ? p.group_of_bit[b] : -1;
+            f[k] = (p.check_async && w < W && b >= GR_STATUS_BITS && b < p.nbits) ? ld_relaxed_sys32(p.dev_flags + b) : 0u;
+            hb[k] = (w < W) ? (p.use_inline ? p.inline_bits[w] : p.host_bits[w]) : 0u;
         }
 #pragma unroll
         for (int k = 0; k < BV_BATCH; ++k) {
             const int w = w0 + k * nwarps;
-            if (w >= p.W) break;  // warp-uniform
-            const int b = w * 32 + lane;
-            bool pend = false;
-            if (gob[k] >= 0 && (f[k] == p.epoch || ((hb[k] >> lane) & 1u))) {
-                pend = p.group_rel_epoch[gob[k]] != p.epoch;
-            } else if (b == 0) {
-                pend = !p.abort_flag;     // complement-coded status bits (R1)
-            } else if (b == 1) {
-                pend = !p.shutdown_flag;
-            }
-            const uint32_t word = __ballot_sync(0xffffffffu, pend);
+            if (w >= W) break;  // warp-uniform
+            uint32_t ready = hb[k] | __ballot_sync(0xffffffffu, f[k] == p.epoch);
+            const int lo = (w == 0) ? GR_STATUS_BITS : 0;                 // tensor bits of word w
+            const int hi = min(32, p.nbits - w * 32);
+            const uint32_t valid = (hi >= 32 ? 0xffffffffu : ((1u << hi) - 1u)) & ~((1u << lo) - 1u);
+            uint32_t word = ready & valid & ~sR[w];
+            if (w == 0) word |= (p.abort_flag ? 0u : 1u) | (p.shutdown_flag ? 0u : 2u);  // complement-coded (R1)
             if (lane == 0) {
                 sL[w] = word;
                 st_relaxed_sys64(my_slot + w, ((uint64_t)p.tag << 32) | word);
@@ -131,11 +130,11 @@ __global__ void __launch_bounds__(BV_THREADS, 4) bitvector_kernel(BvParams p) {
     // LL words (tag|word) read straight from the peers' slots over NVLink, all loads issued
     // before any is consumed; a stale tag (peer not yet in this cycle) is re-polled. ----
     const uint64_t deadline = globaltimer() + p.timeout_ns;
-    for (int w = tid; w < p.W; w += blockDim.x) {
+    for (int w = tid; w < W; w += blockDim.x) {
         uint64_t raw[GR_MAX_RANKS];
 #pragma unroll
         for (int r = 0; r < GR_MAX_RANKS; ++r)
-            raw[r] = (r < p.N && r != p.rank) ? ld_relaxed_sys64(p.slot[r] + (size_t)p.parity * p.W + w) : 0ull;
+            raw[r] = (r < p.N && r != p.rank) ? ld_relaxed_sys64(p.slot[r] + (size_t)p.parity * W + w) : 0ull;
         uint32_t a = sL[w];
 #pragma unroll
         for (int r = 0; r < GR_MAX_RANKS; ++r) {
@@ -143,7 +142,7 @@ __global__ void __launch_bounds__(BV_THREADS, 4) bitvector_kernel(BvParams p) {
             uint64_t x = raw[r];
             while ((uint32_t)(x >> 32) != p.tag) {
                 if (globaltimer() > deadline) { s_timeout = 1; break; }
-                x = ld_relaxed_sys64(p.slot[r] + (size_t)p.parity * p.W + w);
+                x = ld_relaxed_sys64(p.slot[r] + (size_t)p.parity * W + w);
             }
             a &= (uint32_t)x;
         }
@@ -152,27 +151,22 @@ __global__ void __launch_bounds__(BV_THREADS, 4) bitvector_kernel(BvParams p) {
     __syncthreads();
     const uint64_t t_anded = globaltimer();
 
-    // ---- status bits (R1, R13) ----
     int status = ST_OK;
     if (s_timeout) status = ST_TIMEOUT;
-    else if (!(sA[0] & 1u)) status = ST_ABORT;
+    else if (!(sA[0] & 1u)) status = ST_ABORT;      // OR of the ranks' ABORT flags (R1, R13)
     else if (!(sA[0] & 2u)) status = ST_SHUTDOWN;
 
-    // ---- step 3 + grouping: complete groups, ascending ids ----
-    // pass 1: complete(g) = every bit of g's contiguous range set in A. Small groups: one
-    // thread each; groups spanning > GR_SMALL_GROUP_WORDS words: one warp each, the words
-    // checked lane-parallel and combined with __reduce_and_sync.
-    uint32_t *s_cbits = sA + p.W;  // [ceil(G/32)] complete-group bitmask
-    for (int i = tid; i < (p.G + 31) / 32; i += blockDim.x) s_cbits[i] = 0u;
-    __syncthreads();
+    // ---- step 3 + grouping ----
+    // pass 1: complete(g) = every bit of g's contiguous range set in A (released groups never
+    // are: their bits left every L_r). Small groups: a thread each; groups spanning more than
+    // GR_SMALL_GROUP_WORDS words: a warp each, words lane-parallel, __reduce_and_sync.
     auto word_mask = [](int w, int b0, int b1) -> uint32_t {
         const int lo = (w == (b0 >> 5)) ? (b0 & 31) : 0;
         const int hi = (w == ((b1 - 1) >> 5)) ? ((b1 - 1) & 31) : 31;
         return (hi - lo == 31) ? 0xffffffffu : (((1u << (hi - lo + 1)) - 1u) << lo);
     };
     if (status == ST_OK) {
-        for (int g = tid; g < p.G; g += blockDim.x) {
-            if (p.group_rel_epoch[g] == p.epoch) continue;
+        for (int g = tid; g < G; g += blockDim.x) {
             const int b0 = p.group_bit_begin[g], b1 = p.group_bit_end[g];
             if (((b1 - 1) >> 5) - (b0 >> 5) + 1 > GR_SMALL_GROUP_WORDS) continue;
             bool ok = true;
@@ -180,81 +174,91 @@ __global__ void __launch_bounds__(BV_THREADS, 4) bitvector_kernel(BvParams p) {
                 const uint32_t m = word_mask(w, b0, b1);
                 ok = (sA[w] & m) == m;
             }
-            if (ok) atomicOr(&s_cbits[g >> 5], 1u << (g & 31));
+            if (ok) atomicOr(&sC[g >> 5], 1u << (g & 31));
         }
         for (int i = warp; i < p.n_big; i += nwarps) {
             const int g = p.big_groups[i];
-            if (p.group_rel_epoch[g] == p.epoch) continue;  // warp-uniform
             const int b0 = p.group_bit_begin[g], b1 = p.group_bit_end[g];
             bool ok = true;
             for (int w = (b0 >> 5) + lane; w <= ((b1 - 1) >> 5); w += 32) {
                 const uint32_t m = word_mask(w, b0, b1);
                 ok = ok && ((sA[w] & m) == m);
             }
-            if (__reduce_and_sync(0xffffffffu, ok ? 1u : 0u) && lane == 0) atomicOr(&s_cbits[g >> 5], 1u << (g & 31));
+            if (__reduce_and_sync(0xffffffffu, ok ? 1u : 0u) && lane == 0) atomicOr(&sC[g >> 5], 1u << (g & 31));
         }
     }
     __syncthreads();
-    // pass 2: ordered list (block-wide scan over group ids) + chunk prefix sums
-    int run_base = 0, run_ch = 0;
-    if (status == ST_OK) {
-        for (int g0 = 0; g0 < p.G; g0 += blockDim.x) {
-            const int g = g0 + tid;
-            const bool rel = g < p.G && ((s_cbits[g >> 5] >> (g & 31)) & 1u);
-            const int nch = rel ? p.group_nchunks[g] : 0;
-            const long long el = rel ? p.group_elems[g] : 0;
-            const unsigned bal = __ballot_sync(0xffffffffu, rel);
-            const int wpre = __popc(bal & ((1u << lane) - 1u));
-            int x = nch;  // inclusive warp scan of chunk counts
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const int y = __shfl_up_sync(0xffffffffu, x, o);
-                if (lane >= o) x += y;
-            }
-            long long e = el;
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) e += __shfl_down_sync(0xffffffffu, e, o);
-            if (lane == 31) { s_wcnt[warp] = __popc(bal); s_wch[warp] = x; }
-            if (lane == 0 && e) atomicAdd(&s_elems, (unsigned long long)e);
-            __syncthreads();
-            if (warp == 0) {  // exclusive scan of the per-warp totals
-                int c = (lane < nwarps) ? s_wcnt[lane] : 0;
-                int h = (lane < nwarps) ? s_wch[lane] : 0;
-                int ci = c, hi2 = h;
-#pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    const int yc = __shfl_up_sync(0xffffffffu, ci, o);
-                    const int yh = __shfl_up_sync(0xffffffffu, hi2, o);
-                    if (lane >= o) { ci += yc; hi2 += yh; }
-                }
-                if (lane < nwarps) { s_wcnt[lane] = ci - c; s_wch[lane] = hi2 - h; }
-                if (lane == 31) { s_tot_cnt = ci; s_tot_ch = hi2; }
-            }
-            __syncthreads();
-            if (rel) {
-                const int idx = run_base + s_wcnt[warp] + wpre;
-                p.out_released[idx] = g;
-                p.out_cum[idx] = run_ch + s_wch[warp] + (x - nch);
-                p.group_rel_epoch[g] = p.epoch;
-                int32_t *hrel = reinterpret_cast<int32_t *>(reinterpret_cast<uint32_t *>(p.result + 1) + p.W);
-                hrel[idx] = g;
-            }
-            run_base += s_tot_cnt;
-            run_ch += s_tot_ch;
-            __syncthreads();
+    // pass 2 (one pass): thread t owns complete-bitmask words [t*per, (t+1)*per); a block scan
+    // of (count, chunks) gives every released group its slot in the ascending list and its
+    // chunk prefix; the group's bits join the released set.
+    const int per = (Gw + blockDim.x - 1) / blockDim.x;
+    int my_cnt = 0, my_ch = 0;
+    long long my_el = 0;
+    for (int i = tid * per; i < min(Gw, (tid + 1) * per); ++i)
+        for (uint32_t m = sC[i]; m; m &= m - 1) {
+            const int g = i * 32 + __ffs(m) - 1;
+            ++my_cnt;
+            my_ch += p.group_nchunks[g];
+            my_el += p.group_elems[g];
         }
-        if (tid == 0) p.out_cum[run_base] = run_ch;
+    int xc = my_cnt, xh = my_ch;  // inclusive warp scans
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int yc = __shfl_up_sync(0xffffffffu, xc, o), yh = __shfl_up_sync(0xffffffffu, xh, o);
+        if (lane >= o) { xc += yc; xh += yh; }
     }
+    long long e = my_el;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) e += __shfl_down_sync(0xffffffffu, e, o);
+    if (lane == 0 && e) atomicAdd(&s_elems, (unsigned long long)e);
+    if (lane == 31) { s_scan[warp][0] = xc; s_scan[warp][1] = xh; }
+    __syncthreads();
+    if (tid == 0) {
+        int c0 = 0, h0 = 0;
+        for (int i = 0; i < nwarps; ++i) {
+            const int c = s_scan[i][0], h = s_scan[i][1];
+            s_scan[i][0] = c0;
+            s_scan[i][1] = h0;
+            c0 += c;
+            h0 += h;
+        }
+        s_tot[0] = c0;
+        s_tot[1] = h0;
+    }
+    __syncthreads();
+    int32_t *hrel = reinterpret_cast<int32_t *>(reinterpret_cast<uint32_t *>(p.result + 1) + W);
+    {
+        int idx = s_scan[warp][0] + xc - my_cnt, ch = s_scan[warp][1] + xh - my_ch;
+        for (int i = tid * per; i < min(Gw, (tid + 1) * per); ++i)
+            for (uint32_t m = sC[i]; m; m &= m - 1) {
+                const int g = i * 32 + __ffs(m) - 1;
+                p.out_released[idx] = g;
+                p.out_cum[idx] = ch;
+                hrel[idx] = g;
+                ++idx;
+                ch += p.group_nchunks[g];
+                const int b0 = p.group_bit_begin[g], b1 = p.group_bit_end[g];
+                for (int w = b0 >> 5; w <= ((b1 - 1) >> 5); ++w) atomicOr(&sR[w], word_mask(w, b0, b1));
+            }
+    }
+    const int run_base = s_tot[0], run_ch = s_tot[1];
+    if (tid == 0) p.out_cum[run_base] = run_ch;
+    __syncthreads();
 
-    // ---- step_complete: every group released in this step ----
+    // ---- step_complete: every tensor released in this step ----
     bool all = true;
-    for (int g = tid; g < p.G; g += blockDim.x) all = all && (p.group_rel_epoch[g] == p.epoch);
+    for (int w = tid; w < W; w += blockDim.x) {
+        const int lo = (w == 0) ? GR_STATUS_BITS : 0, hi = min(32, p.nbits - w * 32);
+        const uint32_t valid = (hi >= 32 ? 0xffffffffu : ((1u << hi) - 1u)) & ~((1u << lo) - 1u);
+        all = all && ((sR[w] & valid) == valid);
+        p.rel_words[w] = sR[w];
+    }
     const unsigned wall = __reduce_and_sync(0xffffffffu, all ? 1u : 0u);
     if (lane == 0) s_all[warp] = (int)wall;
 
-    // ---- hand the result to the host (pinned, mapped) ----
+    // ---- hand the result over: device copy for the data kernel, pinned copy for the host ----
     uint32_t *hA = reinterpret_cast<uint32_t *>(p.result + 1);
-    for (int w = tid; w < p.W; w += blockDim.x) hA[w] = sA[w];
+    for (int w = tid; w < W; w += blockDim.x) hA[w] = sA[w];
     __syncthreads();
     if (tid == 0) {
         int complete = 1;
@@ -276,7 +280,7 @@ __global__ void __launch_bounds__(BV_THREADS, 4) bitvector_kernel(BvParams p) {
 }
 
 int launch_bitvector(const BvParams &p, void *stream) {
-    const size_t smem = sizeof(uint32_t) * (2 * (size_t)p.W + ((size_t)p.G + 31) / 32);
+    const size_t smem = sizeof(uint32_t) * (3 * (size_t)p.W + ((size_t)p.G + 31) / 32);
     static bool attr_set = false;
     if (!attr_set) {
         cudaFuncSetAttribute(bitvector_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
@@ -378,6 +382,36 @@ template <> struct Buf<float> {
         *reinterpret_cast<float *>(base + idx * ES) = x;
     }
 };
+
+// NVLS: 8 buffer elements reduced in the NVSwitch (multimem.ld_reduce through the multicast
+// address; fp16 accumulates in fp32 inside the switch) and broadcast back (multimem.st).
+__device__ __forceinline__ void mm_ld_reduce8(const __half *mc, float (&x)[8]) {
+    uint32_t r[4];
+    asm volatile("multimem.ld_reduce.relaxed.sys.global.add.acc::f32.v4.f16x2 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]) : "l"(mc) : "memory");
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const float2 f = __half22float2(*reinterpret_cast<const __half2 *>(&r[i]));
+        x[2 * i] = f.x;
+        x[2 * i + 1] = f.y;
+    }
+}
+__device__ __forceinline__ void mm_ld_reduce8(const float *mc, float (&x)[8]) {
+    asm volatile("multimem.ld_reduce.relaxed.sys.global.add.v4.f32 {%0,%1,%2,%3}, [%4];"
+                 : "=f"(x[0]), "=f"(x[1]), "=f"(x[2]), "=f"(x[3]) : "l"(mc) : "memory");
+    asm volatile("multimem.ld_reduce.relaxed.sys.global.add.v4.f32 {%0,%1,%2,%3}, [%4];"
+                 : "=f"(x[4]), "=f"(x[5]), "=f"(x[6]), "=f"(x[7]) : "l"(mc + 4) : "memory");
+}
+__device__ __forceinline__ void mm_st8(__half *mc, const uint4 &v) {
+    asm volatile("multimem.st.relaxed.sys.global.v4.f16x2 [%0], {%1,%2,%3,%4};" ::"l"(mc), "r"(v.x), "r"(v.y),
+                 "r"(v.z), "r"(v.w) : "memory");
+}
+__device__ __forceinline__ void mm_st8(float *mc, const uint4 &a, const uint4 &b) {
+    asm volatile("multimem.st.relaxed.sys.global.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(mc), "r"(a.x), "r"(a.y),
+                 "r"(a.z), "r"(a.w) : "memory");
+    asm volatile("multimem.st.relaxed.sys.global.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(mc + 4), "r"(b.x), "r"(b.y),
+                 "r"(b.z), "r"(b.w) : "memory");
+}
 
 // gradient vector I/O (fp32 or fp16 gradients)
 struct GradRaw { uint4 a, b; };
@@ -519,7 +553,7 @@ __global__ void __launch_bounds__(LC_THREADS, 3) local_kernel(DataParams p) {
 constexpr int XF_THREADS = 512;
 constexpr int XF_CONS = XF_THREADS - 32;
 constexpr int XF_STAGES = 8;  // max ring depth (runtime depth: p.nstages)
-enum { K_PACK = 0, K_RED = 1, K_RS = 2, K_AG = 3, K_STOP = 4 };
+enum { K_PACK = 0, K_RED = 1, K_RS = 2, K_AG = 3, K_NRS = 5, K_STOP = 4 };
 
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -613,7 +647,7 @@ __device__ __forceinline__ float lds_grad1(const char *src, int64_t e, bool f16)
 // the stage (slot_bytes apart), own gradient pieces in the gradient slot (PACK/RED/RS).
 template <typename BT, int KIND>
 __device__ __forceinline__ void xf_consume(const DataParams &p, const XfMeta &m, const char *stage,
-                                           int64_t slot_bytes, const char *gslot, int ct) {
+                                           int64_t slot_bytes, const char *gslot, int ct, char *own_buf) {
     using B = Buf<BT>;
     const int64_t sb = m.sb;
     const bool slow = m.npieces < 0;
@@ -635,7 +669,7 @@ __device__ __forceinline__ void xf_consume(const DataParams &p, const XfMeta &m,
             float acc[8];
             if constexpr (KIND == K_PACK) {
                 lds_grad8(gs + e * esz, pc.f16, acc);
-                B::store(p.buf[p.rank], bi, B::from_f32(acc));
+                B::store(own_buf, bi, B::from_f32(acc));
                 continue;
             } else if constexpr (KIND == K_AG) {
                 B::to_f32(*reinterpret_cast<const typename B::Raw *>(stage + so), acc);
@@ -658,7 +692,7 @@ __device__ __forceinline__ void xf_consume(const DataParams &p, const XfMeta &m,
 #pragma unroll
                 for (int i = 0; i < 8; ++i) acc[i] = acc[i] * p.inv_n;
                 typename B::Raw out = B::from_f32(acc);
-                if constexpr (KIND == K_RS) B::store(p.buf[p.rank], bi, out);
+                if constexpr (KIND == K_RS) B::store(own_buf, bi, out);
             }
             grad_store(pc.g, ti, pc.f16, acc);
         }
@@ -667,7 +701,7 @@ __device__ __forceinline__ void xf_consume(const DataParams &p, const XfMeta &m,
             const int64_t so = (bi - sb) * B::ES;
             auto own = [&]() { return e < pc.body ? lds_grad1(gs, e, pc.f16) : grad_load1(pc.g, ti, pc.f16); };
             if constexpr (KIND == K_PACK) {
-                B::store1(p.buf[p.rank], bi, own());
+                B::store1(own_buf, bi, own());
                 continue;
             }
             float y;
@@ -683,9 +717,58 @@ __device__ __forceinline__ void xf_consume(const DataParams &p, const XfMeta &m,
                     a = (r == 0) ? x : a + x;
                 }
                 y = B::round1(a * p.inv_n);
-                if constexpr (KIND == K_RS) B::store1(p.buf[p.rank], bi, y);
+                if constexpr (KIND == K_RS) B::store1(own_buf, bi, y);
             }
             grad_store1(pc.g, ti, pc.f16, y);
+        }
+    }
+}
+
+// Consumers, NVLS owner: reduce [sb, se) in the switch, x 1/N, round to the buffer precision,
+// broadcast the result into every rank's copy, and unpack it into this rank's gradients.
+// Works on whole 8-element buffer vectors (tensor starts are 8-aligned in the layout, so a
+// tail vector only covers padding beyond the tensor); gradients get only valid elements.
+template <typename BT>
+__device__ __forceinline__ void xf_nvls_reduce(const DataParams &p, const XfMeta &m, int ct) {
+    using B = Buf<BT>;
+    BT *mc = reinterpret_cast<BT *>(p.nvls_mc);
+    const bool slow = m.npieces < 0;
+    const Chunk ch = slow ? p.chunks[m.chunk] : Chunk{0, m.npieces};
+    for (int s = ch.seg_begin; s < ch.seg_end; ++s) {
+        Piece pc;
+        if (slow) {
+            if (!piece_of(p, p.segs[s], m.sb, m.se, pc)) continue;
+        } else {
+            pc = m.pc[s];
+        }
+        const int64_t esz = pc.f16 ? 2 : 4;
+        const bool galigned = ((reinterpret_cast<uintptr_t>(pc.g) + pc.toff * esz) & 15) == 0;
+        const int64_t nv = (pc.n + 7) >> 3;  // buffer vectors (the last may cover padding)
+        constexpr int U = 4;                 // switch reductions in flight per thread
+        for (int64_t v0 = ct; v0 < nv; v0 += (int64_t)XF_CONS * U) {
+            float x[U][8];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int64_t v = v0 + (int64_t)u * XF_CONS;
+                if (v < nv) mm_ld_reduce8(mc + pc.lo + 8 * v, x[u]);
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int64_t v = v0 + (int64_t)u * XF_CONS;
+                if (v >= nv) continue;
+#pragma unroll
+                for (int i = 0; i < 8; ++i) x[u][i] = x[u][i] * p.inv_n;
+                typename B::Raw out = B::from_f32(x[u]);
+                if constexpr (sizeof(BT) == 2) mm_st8(mc + pc.lo + 8 * v, out.a);
+                else mm_st8(reinterpret_cast<float *>(mc) + pc.lo + 8 * v, reinterpret_cast<const uint4 *>(&out)[0],
+                            reinterpret_cast<const uint4 *>(&out)[1]);
+                const int64_t e = 8 * v;
+                if (galigned && e + 8 <= pc.n) {
+                    grad_store(pc.g, pc.toff + e, pc.f16, x[u]);
+                } else {
+                    for (int i = 0; i < 8 && e + i < pc.n; ++i) grad_store1(pc.g, pc.toff + e + i, pc.f16, x[u][i]);
+                }
+            }
         }
     }
 }
@@ -717,7 +800,8 @@ __global__ void __maxnreg__(96) xfer_kernel(DataParams p) {
     const int nrel = p.info->n_released;
     const int total = p.info->total_chunks;
     // algorithm chosen on the device from the released message size (same rule on every rank)
-    const int ALGO = (p.info->elems * B::ES <= p.one_shot_max_bytes) ? ALGO_ONESHOT : ALGO_TWOSHOT;
+    const int ALGO = (p.info->elems * B::ES <= p.one_shot_max_bytes) ? ALGO_ONESHOT
+                     : (p.nvls_mc ? ALGO_NVLS : ALGO_TWOSHOT);
     const bool cached = nrel <= XF_RCACHE;
     if (cached)
         for (int j = tid; j < nrel; j += blockDim.x) {
@@ -803,11 +887,12 @@ __global__ void __maxnreg__(96) xfer_kernel(DataParams p) {
                 }
                 if (src) {  // peer copies: lane r fetches rank r's sub-tile
                     const uint32_t bytes = (uint32_t)(((se - sb) * B::ES + 15) & ~(int64_t)15);
-                    const bool mine = src == 1 ? (lane < p.N && lane != p.rank) : (lane == owner);
+                    const bool mine = src == 1 ? (lane < p.N && lane != p.rank) : (src == 2 ? lane == owner : lane == 0);
                     if (mine) {
                         const int slot = (src == 1) ? (lane < p.rank ? lane : lane - 1) : 0;
+                        const char *from = (src == 3) ? p.nvls_uc : p.buf[lane];  // 3: own NVLS copy
                         mbar_expect_tx(bar, bytes);
-                        bulk_g2s(dst + (size_t)slot * p.slot_bytes_red, p.buf[lane] + sb * B::ES, bytes, bar);
+                        bulk_g2s(dst + (size_t)slot * p.slot_bytes_red, from + sb * B::ES, bytes, bar);
                     }
                 }
                 __syncwarp();
@@ -847,15 +932,19 @@ __global__ void __maxnreg__(96) xfer_kernel(DataParams p) {
                 if (ALGO == ALGO_ONESHOT || c % p.N == p.rank) {
                     uint64_t *tr = p.trace ? p.trace + ((size_t)total + i1) * 4 : nullptr;
                     if (tr && lane == 0) tr[0] = globaltimer();
-                    // one-shot also waits for its own PACK(c): RED overwrites g after PACK read it
-                    ok = wait_flags(p.pack_flag[p.rank] + (size_t)c * p.N, 1, p.N, ALGO == ALGO_ONESHOT ? -1 : p.rank, 1);
+                    // one-shot and NVLS also wait for their own PACK(c) (RED overwrites g after
+                    // PACK read it; the switch reads this rank's copy too)
+                    ok = wait_flags(p.pack_flag[p.rank] + (size_t)c * p.N, 1, p.N, ALGO == ALGO_TWOSHOT ? p.rank : -1, 1);
                     if (!ok) break;
                     if (tr && lane == 0) tr[1] = globaltimer();
-                    produce(ALGO == ALGO_ONESHOT ? K_RED : K_RS, total + i1, c, p.sub_red, 1, -1, true);
+                    // NVLS: no staging, the consumers' own multimem loads are in flight -> whole chunk
+                    if (ALGO == ALGO_NVLS) produce(K_NRS, total + i1, c, 1 << 30, 0, -1, false);
+                    else produce(ALGO == ALGO_ONESHOT ? K_RED : K_RS, total + i1, c, p.sub_red, 1, -1, true);
                 }
             }
-            // AG(k-L2) (two-shot): pull the owner's reduced chunk
-            if (ALGO == ALGO_TWOSHOT) {
+            // AG(k-L2) (two-shot: pull the owner's reduced chunk; NVLS: it is already in this
+            // rank's copy, written by the owner's multicast store)
+            if (ALGO != ALGO_ONESHOT) {
                 const int i2 = k - lag2;
                 if (i2 >= 0 && i2 < total) {
                     const int c = chunk_of(i2);
@@ -866,7 +955,7 @@ __global__ void __maxnreg__(96) xfer_kernel(DataParams p) {
                         ok = wait_flags(p.rs_flag[p.rank] + c, 0, 1, -1, 2);
                         if (!ok) break;
                         if (tr && lane == 0) tr[1] = globaltimer();
-                        produce(K_AG, 2 * total + i2, c, p.sub_ag, 2, owner, false);
+                        produce(K_AG, 2 * total + i2, c, p.sub_ag, ALGO == ALGO_NVLS ? 3 : 2, owner, false);
                     }
                 }
             }
@@ -887,21 +976,23 @@ __global__ void __maxnreg__(96) xfer_kernel(DataParams p) {
             if (kind == K_STOP) break;
             const int item = m.item, c = m.chunk, last = m.last;
             const char *st = xsm + (size_t)stage * stage_bytes;
-            if (kind == K_PACK) xf_consume<BT, K_PACK>(p, m, st, 0, st, ct);
-            else if (kind == K_RED) xf_consume<BT, K_RED>(p, m, st, p.slot_bytes_red, st + gslot_off, ct);
-            else if (kind == K_RS) xf_consume<BT, K_RS>(p, m, st, p.slot_bytes_red, st + gslot_off, ct);
-            else xf_consume<BT, K_AG>(p, m, st, 0, st, ct);
+            char *own = ALGO == ALGO_NVLS ? p.nvls_uc : p.buf[p.rank];  // this rank's fusion buffer
+            if (kind == K_PACK) xf_consume<BT, K_PACK>(p, m, st, 0, st, ct, own);
+            else if (kind == K_RED) xf_consume<BT, K_RED>(p, m, st, p.slot_bytes_red, st + gslot_off, ct, own);
+            else if (kind == K_RS) xf_consume<BT, K_RS>(p, m, st, p.slot_bytes_red, st + gslot_off, ct, own);
+            else if (kind == K_NRS) xf_nvls_reduce<BT>(p, m, ct);
+            else xf_consume<BT, K_AG>(p, m, st, 0, st, ct, own);
             // the stage is free once every consumer warp has read it
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[stage]);
-            if (last && (kind == K_PACK || kind == K_RS)) {  // chunk done: publish its flag
+            if (last && (kind == K_PACK || kind == K_RS || kind == K_NRS)) {  // chunk done: publish its flag
                 consumer_sync();
                 if (ct == 0) {
                     fence_sys();
-                    if (kind == K_RS) {
+                    if (kind == K_RS || kind == K_NRS) {
                         for (int q = 0; q < p.N; ++q)
                             if (q != p.rank) st_relaxed_sys32(p.rs_flag[q] + c, p.epoch);
-                    } else if (ALGO == ALGO_TWOSHOT) {
+                    } else if (ALGO == ALGO_TWOSHOT || ALGO == ALGO_NVLS) {  // the owner (NVLS: possibly this rank)
                         st_relaxed_sys32(p.pack_flag[c % p.N] + (size_t)c * p.N + p.rank, p.epoch);
                     } else {  // every rank, this one included: RED(c) must not overwrite g before PACK(c) read it
                         for (int q = 0; q < p.N; ++q) st_relaxed_sys32(p.pack_flag[q] + (size_t)c * p.N + p.rank, p.epoch);

@@ -25,6 +25,7 @@
 
 #include "gr.h"
 #include "gr_internal.h"
+#include "gr_nvls.h"
 
 using gr::Chunk;
 using gr::Seg;
@@ -86,11 +87,10 @@ struct gr_ctx {
     Seg *d_segs = nullptr;
     Chunk *d_chunks = nullptr;
     int64_t *d_cbeg = nullptr, *d_cend = nullptr;
-    int32_t *d_tob = nullptr, *d_gob = nullptr, *d_gbb = nullptr, *d_gbe = nullptr, *d_gnch = nullptr,
-            *d_gcb = nullptr;
+    int32_t *d_gbb = nullptr, *d_gbe = nullptr, *d_gnch = nullptr, *d_gcb = nullptr;
     int64_t *d_gel = nullptr;
     int32_t *d_big = nullptr;
-    uint32_t *d_grel = nullptr;
+    uint32_t *d_relw = nullptr, *d_hbits_dev = nullptr;
     uint64_t *d_ptr = nullptr;
     int32_t *d_rel_ring = nullptr, *d_cum_ring = nullptr;
     gr::DevCycle *d_info_ring = nullptr;
@@ -118,11 +118,17 @@ struct gr_ctx {
     uint64_t seq = 0;
     bool step_complete = false;
     bool need_compute_fence = false;
+    bool step_fresh = true;   // next gr_step is the first cycle of a step
+    bool async_used = false;  // gr_mark_ready_async used in this step
     std::atomic<bool> ptr_dirty{false};
     int32_t abort_flag = 0, shutdown_flag = 0;
     int sticky = 0;
     int last_algo = GR_ALGO_NONE;
     std::string err = "no error";
+
+    // NVLS multicast fusion buffer (optional; see gr_nvls.cpp)
+    gr::Nvls nvls;
+    std::string nvls_why = "not attempted";
 
     // tracing (GR_TRACE)
     std::string trace_path;
@@ -336,16 +342,15 @@ int setup_device(gr_ctx *c) {
     RC(upload(c, &c->d_chunks, c->chunks));
     RC(upload(c, &c->d_cbeg, c->chunk_begin));
     RC(upload(c, &c->d_cend, c->chunk_end));
-    RC(upload(c, &c->d_tob, c->tensor_of_bit));
-    RC(upload(c, &c->d_gob, c->group_of_bit));
     RC(upload(c, &c->d_gbb, c->gbit_begin));
     RC(upload(c, &c->d_gbe, c->gbit_end));
     RC(upload(c, &c->d_gnch, c->gnchunks));
     RC(upload(c, &c->d_gcb, c->gchunk_begin));
     RC(upload(c, &c->d_gel, c->gelems));
     RC(upload(c, &c->d_big, c->big_groups));
-    CK(c, cudaMalloc((void **)&c->d_grel, sizeof(uint32_t) * c->G));
-    CK(c, cudaMemset(c->d_grel, 0, sizeof(uint32_t) * c->G));
+    CK(c, cudaMalloc((void **)&c->d_relw, sizeof(uint32_t) * c->W));
+    CK(c, cudaMemset(c->d_relw, 0, sizeof(uint32_t) * c->W));
+    CK(c, cudaMalloc((void **)&c->d_hbits_dev, sizeof(uint32_t) * c->W));
     CK(c, cudaMalloc((void **)&c->d_ptr, sizeof(uint64_t) * c->T));
     CK(c, cudaMalloc((void **)&c->d_rel_ring, sizeof(int32_t) * GR_SLOT_RING * (size_t)c->G));
     CK(c, cudaMalloc((void **)&c->d_cum_ring, sizeof(int32_t) * GR_SLOT_RING * (size_t)(c->G + 1)));
@@ -420,6 +425,27 @@ int setup_device(gr_ctx *c) {
         CK(c, cudaIpcOpenMemHandle(&p, all[r], cudaIpcMemLazyEnablePeerAccess));
         c->peer_symm[r] = (char *)p;
     }
+
+    // NVLS (NEXT-1): in-switch reduction for large messages. It moves S(1+1/N) NVLink bytes per
+    // direction against 2S(N-1)/N for two-shot; measured at N = 4 it is still slower than
+    // two-shot, so it defaults on only from N = 8. GR_NVLS=1 forces it from
+    // N = 2, GR_NVLS=0 turns it off.
+    if (c->N > 1) {
+        const char *e = getenv("GR_NVLS");
+        const bool want = e ? atoi(e) != 0 : c->N >= 8;
+        auto ag = [c](const void *snd, void *rcv, size_t n) { return allgather(c, snd, rcv, n); };
+        int32_t w = want ? 1 : 0;
+        std::vector<int32_t> ws(c->N);
+        RC(allgather(c, &w, ws.data(), sizeof w));
+        bool all = true;
+        for (int v : ws) all = all && v;
+        if (all) {
+            if (gr::nvls_setup(c->nvls, c->rank, c->N, c->dev, 2 * c->buf_parity_bytes, ag, c->nvls_why) == 0)
+                c->nvls_why = "enabled";
+        } else {
+            c->nvls_why = "disabled (GR_NVLS / world size)";
+        }
+    }
     return GR_OK;
 }
 
@@ -430,9 +456,10 @@ void free_all(gr_ctx *c) {
     if (c->s_data) cudaStreamSynchronize(c->s_data);
     for (int r = 0; r < c->N; ++r)
         if (r != c->rank && c->peer_symm[r]) cudaIpcCloseMemHandle(c->peer_symm[r]);
+    gr::nvls_free(c->nvls);
     cudaFree(c->symm);
-    void *dptrs[] = {c->d_segs, c->d_chunks, c->d_cbeg, c->d_cend, c->d_tob, c->d_gob, c->d_gbb, c->d_gbe, c->d_gnch, c->d_gcb,
-                     c->d_gel, c->d_big, c->d_grel, c->d_ptr, c->d_rel_ring, c->d_cum_ring, c->d_info_ring, c->d_counters,
+    void *dptrs[] = {c->d_segs, c->d_chunks, c->d_cbeg, c->d_cend, c->d_gbb, c->d_gbe, c->d_gnch, c->d_gcb,
+                     c->d_gel, c->d_big, c->d_relw, c->d_hbits_dev, c->d_ptr, c->d_rel_ring, c->d_cum_ring, c->d_info_ring, c->d_counters,
                      c->d_flags, c->d_trace};
     for (void *p : dptrs) cudaFree(p);
     cudaFreeHost(c->h_bits);
@@ -609,6 +636,7 @@ int gr_mark_ready_async(gr_ctx *c, int32_t rank, int32_t t, void *dev_ptr, void 
     if (!c->dry && !c->write_value32) return fail(c, GR_ECUDA, "cuStreamWriteValue32 unavailable");
     int rc = mark_common(c, rank, t, dev_ptr);
     if (rc) return rc;
+    c->async_used = true;
     CUresult r = c->write_value32((CUstream)stream, (CUdeviceptr)(c->d_flags + c->bit_of[t]), c->epoch, 0);
     if (r != CUDA_SUCCESS) {
         c->marked[t] = 0;
@@ -639,7 +667,7 @@ int gr_step(gr_ctx *c, int32_t *released, gr_cycle_info *info, uint32_t *global_
     }
     uint32_t epoch;
     int32_t abort_flag, shutdown_flag;
-    bool p_inline = false;
+    bool p_inline = false, step_fresh = false, async_used = false;
     uint32_t inline_bits[GR_BV_INLINE_WORDS];
     {
         std::lock_guard<std::mutex> lk(c->mu);
@@ -650,6 +678,9 @@ int gr_step(gr_ctx *c, int32_t *released, gr_cycle_info *info, uint32_t *global_
             c->need_compute_fence = false;
         }
         epoch = c->epoch;
+        step_fresh = c->step_fresh;
+        c->step_fresh = false;
+        async_used = c->async_used;
         if (c->W <= GR_BV_INLINE_WORDS) {  // snapshot the host mark bits into the launch itself
             p_inline = true;
             for (int w = 0; w < c->W; ++w) inline_bits[w] = __atomic_load_n(&c->h_bits[w], __ATOMIC_ACQUIRE);
@@ -659,17 +690,17 @@ int gr_step(gr_ctx *c, int32_t *released, gr_cycle_info *info, uint32_t *global_
     }
 
     gr::BvParams p{};
-    p.host_bits = c->d_hbits;
+    p.host_bits = c->d_hbits_dev;
     p.dev_flags = c->d_flags;
-    p.tensor_of_bit = c->d_tob;
-    p.group_of_bit = c->d_gob;
+    p.new_step = step_fresh;
+    p.check_async = async_used;
     p.group_bit_begin = c->d_gbb;
     p.group_bit_end = c->d_gbe;
     p.group_nchunks = c->d_gnch;
     p.group_elems = c->d_gel;
     p.big_groups = c->d_big;
     p.n_big = (int32_t)c->big_groups.size();
-    p.group_rel_epoch = c->d_grel;
+    p.rel_words = c->d_relw;
     for (int r = 0; r < c->N; ++r) p.slot[r] = reinterpret_cast<uint64_t *>(c->peer_symm[r] + c->off_slot);
     p.out_released = c->d_rel_ring + (size_t)slot * c->G;
     p.out_cum = c->d_cum_ring + (size_t)slot * (c->G + 1);
@@ -697,6 +728,8 @@ int gr_step(gr_ctx *c, int32_t *released, gr_cycle_info *info, uint32_t *global_
         evb = get_ev_pair(c);
         CK(c, cudaEventRecord(evb.first, c->s_coord));
     }
+    if (!p_inline)  // larger bitvectors: one DMA of the pinned mark bits, stream-ordered before the kernel
+        CK(c, cudaMemcpyAsync(c->d_hbits_dev, c->h_bits, sizeof(uint32_t) * c->W, cudaMemcpyHostToDevice, c->s_coord));
     int lrc = gr::launch_bitvector(p, c->s_coord);
     if (lrc) return fail(c, GR_ECUDA, "bitvector launch: %s", cudaGetErrorString((cudaError_t)lrc));
     if (c->timing) {
@@ -718,6 +751,8 @@ int gr_step(gr_ctx *c, int32_t *released, gr_cycle_info *info, uint32_t *global_
         d.info = p.out_info;
         d.dev_ptr = c->d_ptr;
         const int par = (int)(epoch & 1);
+        d.nvls_uc = c->nvls.enabled ? reinterpret_cast<char *>(c->nvls.ucva) + (size_t)par * c->buf_parity_bytes : nullptr;
+        d.nvls_mc = c->nvls.enabled ? reinterpret_cast<char *>(c->nvls.mcva) + (size_t)par * c->buf_parity_bytes : nullptr;
         for (int r = 0; r < c->N; ++r) {
             char *base = c->peer_symm[r];
             d.buf[r] = base + c->off_buf + (size_t)par * c->buf_parity_bytes;
@@ -812,7 +847,9 @@ int gr_step(gr_ctx *c, int32_t *released, gr_cycle_info *info, uint32_t *global_
     if (n > 0) {
         const int64_t msg_bytes = rel_elems * (c->buf_f16 ? 2 : 4);
         c->last_algo = c->N == 1 ? gr::ALGO_LOCAL
-                                 : (msg_bytes <= c->one_shot_max_bytes ? gr::ALGO_ONESHOT : gr::ALGO_TWOSHOT);
+                                 : (msg_bytes <= c->one_shot_max_bytes
+                                        ? gr::ALGO_ONESHOT
+                                        : (c->nvls.enabled ? gr::ALGO_NVLS : gr::ALGO_TWOSHOT));
         c->stats.released_elems += rel_elems;
     }
     const int complete = c->h_res->step_complete;
@@ -864,6 +901,8 @@ static int start_next_step(gr_ctx *c) {
         c->stats.steps++;
         std::fill(c->marked.begin(), c->marked.end(), 0);
         memset(c->h_bits, 0, sizeof(uint32_t) * (size_t)c->W);  // no bitvector kernel is in flight
+        c->step_fresh = true;
+        c->async_used = false;
     }
     return GR_OK;
 }
@@ -946,6 +985,17 @@ int gr_query(gr_ctx *c, int32_t kind, void *out, size_t bytes) {
         case GR_Q_NCHUNKS: return put(&c->C, sizeof(int32_t));
         case GR_Q_STATS: return put(&c->stats, sizeof(gr_stats));
         case GR_Q_LAST_ALGO: return put(&c->last_algo, sizeof(int32_t));
+        case GR_Q_NVLS: {
+            const int32_t v = c->nvls.enabled ? 1 : 0;
+            return put(&v, sizeof v);
+        }
+        case GR_Q_NVLS_WHY: {  // NUL-terminated, truncated to `bytes`
+            if (bytes == 0) return fail(c, GR_EINVAL, "gr_query: zero-size buffer");
+            const size_t n = std::min(bytes - 1, c->nvls_why.size());
+            memcpy(out, c->nvls_why.data(), n);
+            static_cast<char *>(out)[n] = 0;
+            return GR_OK;
+        }
         default: return fail(c, GR_EINVAL, "unknown query %d", kind);
     }
 }

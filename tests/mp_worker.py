@@ -31,6 +31,7 @@ def main():
     import torch.distributed as dist
 
     from paper_1909_11150_b200 import GR_F16, GR_F32, Context, make_allgather
+    from paper_1909_11150_b200.binding import GR_Q_NVLS
     from tests.parity_lib import run_case_on_rank
     from workloads import cfg1_case, fcn220m
     from workloads.schedules import Case, random_mark_schedule, random_partition, reverse_layer_schedule
@@ -54,9 +55,12 @@ def main():
                       one_shot_max_bytes=args.one_shot_max_bytes if osm is None else osm,
                       chunk_elems=chunk or args.chunk_elems, timeout_ms=20000, allgather=ag)
         ok = True
+        nvls, why = ctx.nvls()
+        if os.environ.get("GR_NVLS") == "1" and not nvls:
+            raise RuntimeError(f"GR_NVLS=1 but NVLS is not enabled: {why}")
         try:
             _log, h = run_case_on_rank(ctx, case, rank, seed, dev, buf == "f16", grad_f16, kind,
-                                       max_cycles=max_cycles)
+                                       max_cycles=max_cycles, exact=not nvls)
         except AssertionError as e:
             ok = False
             h = "FAIL"
@@ -102,7 +106,8 @@ def main():
     tot = [None] * N
     dist.all_gather_object(tot, failures)
     if rank == 0:
-        print(f"mp_worker suite={args.suite} N={N} cases={ncase} failures={sum(tot)}", flush=True)
+        print(f"mp_worker suite={args.suite} N={N} cases={ncase} failures={sum(tot)} "
+              f"GR_NVLS={os.environ.get('GR_NVLS', 'default')}", flush=True)
     dist.destroy_process_group()
     sys.exit(1 if sum(tot) else 0)
 

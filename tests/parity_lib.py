@@ -53,13 +53,16 @@ def check_schedule(log, ref, where=""):
             f"{where}: cycle {c} released gpu={log.released[c]} oracle={ref.released[c]}"
 
 
-def check_values(out_np, gs, N, buffer_f16: bool, grad_f16_t: bool, where=""):
+def check_values(out_np, gs, N, buffer_f16: bool, grad_f16_t: bool, where="", exact: bool = True):
+    """exact=False (NVLS: the switch accumulates in its own order) keeps only the north-star
+    tolerance; integer payloads are exact in any order and are checked with exact=True."""
     emu = oracle.emulate(gs, buffer_f16, grad_f16_t)
     ref = oracle.reduce_f64(gs)
     out = out_np.astype(np.float32)
     bad = np.nonzero(out.view(np.uint32) != emu.view(np.uint32))[0]
-    assert bad.size == 0, (f"{where}: {bad.size} elements differ from the oracle emulation, first "
-                           f"i={bad[0]} gpu={out[bad[0]]!r} emu={emu[bad[0]]!r}")
+    if exact:
+        assert bad.size == 0, (f"{where}: {bad.size} elements differ from the oracle emulation, first "
+                               f"i={bad[0]} gpu={out[bad[0]]!r} emu={emu[bad[0]]!r}")
     o64 = out.astype(np.float64)
     stack = np.stack(gs).astype(np.float64)
     if buffer_f16:
@@ -73,7 +76,7 @@ def check_values(out_np, gs, N, buffer_f16: bool, grad_f16_t: bool, where=""):
 
 
 def run_case_on_rank(ctx, case, r, seed, device, buffer_f16: bool, grad_f16=None, kind="uniform",
-                     max_cycles=None, async_stream=None):
+                     max_cycles=None, async_stream=None, exact: bool = True):
     """Replay `case` on rank r through the C ABI and check it against the oracle.
     Returns (log, sha256 of all output gradients) for the cross-rank comparison."""
     import torch
@@ -97,5 +100,6 @@ def run_case_on_rank(ctx, case, r, seed, device, buffer_f16: bool, grad_f16=None
             continue
         idx = sample_indices(out.size, seed * 7919 + t)
         gs = host_inputs(case.numel, case.N, seed, t, f16, kind, idx)
-        check_values(out[idx], gs, case.N, buffer_f16, f16, where=f"rank {r} seed {seed} tensor {t}")
+        check_values(out[idx], gs, case.N, buffer_f16, f16, where=f"rank {r} seed {seed} tensor {t}",
+                     exact=exact or kind == "int")
     return log, h.hexdigest()

@@ -188,8 +188,8 @@ def test_fcn220m_n1_full_size(gpu):
         ctx.gr_finalize()
 
 
-def _torchrun(n, *args, timeout=900):
-    env = dict(os.environ, PYTHONPATH=ROOT)
+def _torchrun(n, *args, timeout=900, env_extra=None):
+    env = dict(os.environ, PYTHONPATH=ROOT, **(env_extra or {}))
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
            "--master-addr", "127.0.0.1", "--master-port", str(29500 + n), os.path.join(ROOT, "tests", "mp_worker.py"),
            *args]
@@ -217,3 +217,14 @@ def test_multi_gpu_fcn220m(n):
     if gpu_count() < n:
         pytest.skip(f"needs {n} GPUs")
     assert _torchrun(n, "--suite", "fcn", "--seeds", "5:6") == 0
+
+
+@pytest.mark.parametrize("n", [2, 4, 8])
+def test_multi_gpu_nvls(n):
+    """NVLS (in-switch reduction) forced on: edge shapes and the full fcn220m set; values
+    within the north-star tolerance (the switch's accumulation order is its own), integer
+    payloads bit-exact, replicas bitwise identical."""
+    if gpu_count() < n:
+        pytest.skip(f"needs {n} GPUs")
+    assert _torchrun(n, "--suite", "edge", "--seeds", "0:3", env_extra={"GR_NVLS": "1"}) == 0
+    assert _torchrun(n, "--suite", "fcn", "--seeds", "7:8", env_extra={"GR_NVLS": "1"}) == 0

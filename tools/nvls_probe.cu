@@ -28,7 +28,8 @@ __global__ void red_kernel(const float *mc, float *out, int n) {
     }
 }
 
-int main() {
+int main(int argc, char **argv) {
+    const bool try_fabric = argc > 1;
     CU(cuInit(0));
     int ndev = 0;
     cuDeviceGetCount(&ndev);
@@ -51,7 +52,7 @@ int main() {
     CU(cuMulticastCreate(&mc, &mp));
     int fd = -1;
     CUW(cuMemExportToShareableHandle(&fd, mc, CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR, 0));
-    {   // fabric export of a multicast object
+    if (try_fabric) {   // fabric export of a multicast object
         CUmulticastObjectProp mp2 = mp;
         mp2.handleTypes = CU_MEM_HANDLE_TYPE_FABRIC;
         CUmemGenericAllocationHandle mc2;
@@ -63,10 +64,9 @@ int main() {
             cuMemRelease(mc2);
         }
     }
-    for (int i = 0; i < 2; ++i) CU(cuMulticastAddDevice(mc, dev[i]));
     CUmemGenericAllocationHandle phys[2];
     CUdeviceptr uc[2], mcva[2];
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < 2; ++i) {  // physical memory first (variants), then add devices
         CU(cuCtxSetCurrent(ctx[i]));
         CUmemAllocationProp pp;
         memset(&pp, 0, sizeof pp);
@@ -74,7 +74,21 @@ int main() {
         pp.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
         pp.location.id = i;
         pp.requestedHandleTypes = CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR;
-        CU(cuMemCreate(&phys[i], size, &pp, 0));
+        size_t g2 = 0;
+        CUW(cuMemGetAllocationGranularity(&g2, &pp, CU_MEM_ALLOC_GRANULARITY_RECOMMENDED));
+        printf("alloc granularity %zu\n", g2);
+        CUresult r = cuMemCreate(&phys[i], size, &pp, 0);
+        printf("cuMemCreate(POSIX_FD) dev %d -> %d\n", i, (int)r);
+        if (r != CUDA_SUCCESS) {
+            pp.requestedHandleTypes = CU_MEM_HANDLE_TYPE_NONE;
+            r = cuMemCreate(&phys[i], size, &pp, 0);
+            printf("cuMemCreate(NONE) dev %d -> %d\n", i, (int)r);
+            if (r != CUDA_SUCCESS) return 1;
+        }
+    }
+    for (int i = 0; i < 2; ++i) CU(cuMulticastAddDevice(mc, dev[i]));
+    for (int i = 0; i < 2; ++i) {
+        CU(cuCtxSetCurrent(ctx[i]));
         CU(cuMulticastBindMem(mc, 0, phys[i], 0, size, 0));
         CUmemAccessDesc ad;
         ad.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
