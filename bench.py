@@ -441,6 +441,28 @@ def run_extras(args, ctx, grads, ptrs, tensor_order, f, N, rank, local, dev, com
                            "marks": "gr_mark_ready_async on the compute stream after each layer"}
     ctx2.gr_finalize()
 
+    # ---- NEXT-2 epilogue cost: the same step with the fused ||g||^2 / non-finite statistics ----
+    batch = ctx.prepare_batch(tensor_order, [ptrs[t] for t in tensor_order])
+
+    def step_stats():
+        ctx.gr_mark_ready_prepared(batch)
+        ctx.gr_step()
+        ctx.gr_wait_async()
+
+    ctx.gr_enable_grad_stats(True)
+    for _ in range(3):
+        step_stats()
+    barrier()
+    torch.cuda.synchronize()
+    a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a0.record(compute)
+    for _ in range(10):
+        step_stats()
+    a1.record(compute)
+    torch.cuda.synchronize()
+    out["ms_per_step_with_grad_stats"] = round(max_over_ranks(a0.elapsed_time(a1) / 10), 4)
+    ctx.gr_enable_grad_stats(False)
+
     # ---- bitvector-only cycle latency (no tensor ready: pure coordination round) ----
     lat = []
     barrier()

@@ -168,6 +168,22 @@ int gr_wait_async(gr_ctx *ctx);
  * status bit for the following cycles (PAPER.md:130 reserved status bits). */
 int gr_set_status(gr_ctx *ctx, int32_t abort_flag, int32_t shutdown_flag);
 
+/* Gradient statistics epilogue (PAPER.md:281 LARS, PAPER.md:283
+ * adaptive loss scaling), fused into the unpack: while writing the reduced gradients the kernels
+ * accumulate, per tensor, the sum of squares of the stored values (fp64 accumulator; LARS's
+ * ||g||^2) and a flag that is 1 if any stored value is Inf/NaN (loss-scale overflow). Every rank
+ * holds the full reduced gradient, so every rank gets the full statistics without extra
+ * communication. Reset at the first cycle of each step.
+ * gr_enable_grad_stats — LOCAL: on != 0 enables (allocates T doubles + one int32).
+ * gr_grad_stats — LOCAL: after gr_wait (or a host sync), copy the current step's statistics
+ *   to host memory (sumsq_host: T doubles, nonfinite_host: one int32; both nullable) and/or
+ *   return the library-owned device arrays (sumsq_dev / nonfinite_dev, nullable) for a GPU
+ *   optimizer (valid until the next step's first gr_step, stream-ordered after gr_wait_async).
+ *   GR_ESTATE if statistics are not enabled. */
+int gr_enable_grad_stats(gr_ctx *ctx, int32_t on);
+int gr_grad_stats(gr_ctx *ctx, double *sumsq_host, int32_t *nonfinite_host, void **sumsq_dev,
+                  void **nonfinite_dev);
+
 /* gr_finalize — COLLECTIVE at the application level (no communication, but
  * peers must not be mid-cycle). Frees everything; ctx may be NULL. */
 int gr_finalize(gr_ctx *ctx);

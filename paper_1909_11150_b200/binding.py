@@ -76,6 +76,8 @@ def _load():
         "gr_set_timing": ([p, i32], ctypes.c_int),
         "gr_reset_stats": ([p], ctypes.c_int),
         "gr_bench_spin": ([i64, i32, p], ctypes.c_int),
+        "gr_enable_grad_stats": ([p, i32], ctypes.c_int),
+        "gr_grad_stats": ([p, p, p, p, p], ctypes.c_int),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)
@@ -86,7 +88,8 @@ def _load():
 
 lib = _load()
 EXPORTED = ("gr_init", "gr_mark_ready", "gr_mark_ready_batch", "gr_mark_ready_async", "gr_step", "gr_wait", "gr_wait_async", "gr_set_status",
-            "gr_finalize", "gr_last_error", "gr_query", "gr_set_timing", "gr_reset_stats", "gr_bench_spin")
+            "gr_finalize", "gr_last_error", "gr_query", "gr_set_timing", "gr_reset_stats", "gr_bench_spin",
+            "gr_enable_grad_stats", "gr_grad_stats")
 
 
 def _check(rc: int, ctx=None):
@@ -212,6 +215,17 @@ class Context:
         s = GrStats()
         _check(lib.gr_query(self._ctx, GR_Q_STATS, ctypes.byref(s), ctypes.sizeof(s)), self._ctx)
         return s
+
+    def gr_enable_grad_stats(self, on: bool = True):
+        return _check(lib.gr_enable_grad_stats(self._ctx, int(on)), self._ctx)
+
+    def gr_grad_stats(self):
+        """(sum of squares per tensor [list of float], non-finite flag) of the last step."""
+        ss = (ctypes.c_double * self.T)()
+        nf = ctypes.c_int32()
+        _check(lib.gr_grad_stats(self._ctx, ctypes.cast(ss, ctypes.c_void_p), ctypes.byref(nf), None, None),
+               self._ctx)
+        return list(ss), bool(nf.value)
 
     def set_timing(self, on: bool):
         _check(lib.gr_set_timing(self._ctx, int(on)), self._ctx)

@@ -109,6 +109,8 @@ struct DataParams {
     int64_t sub_red, sub_ag, sub_pack; // staged sub-tile (elements) for reduce / all-gather / pack items
     int32_t lag1, lag2;                // queue lags (in released chunks) of reduce / all-gather items
     int64_t one_shot_max_bytes;        // N>1: messages up to this many buffer bytes go one-shot
+    double *sumsq;                     // optional [T]: sum of squares of the reduced gradient (NEXT-2)
+    int32_t *nonfinite;                // optional: set to 1 if any reduced value is Inf/NaN
     int32_t rank, N;
     uint32_t epoch;
     float inv_n;

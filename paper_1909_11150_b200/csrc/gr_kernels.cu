@@ -458,6 +458,42 @@ __device__ __forceinline__ float grad_load1(const char *g, int64_t idx, bool f16
     return f16 ? __half2float(*reinterpret_cast<const __half *>(g + idx * 2))
                : *reinterpret_cast<const float *>(g + idx * 4);
 }
+// NEXT-2 epilogue (LARS needs ||g||^2 per tensor, dynamic loss scaling needs a non-finite
+// flag): accumulate the squares of the values as stored in the gradient
+// tensor and note any Inf/NaN. Per thread in registers; one warp reduction + atomic per piece.
+struct GradStat {
+    double ss = 0.0;
+    unsigned nf = 0;
+    __device__ __forceinline__ void add8(const float (&x)[8], bool f16) {
+        float s = 0.f;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const float v = f16 ? __half2float(__float2half_rn(x[i])) : x[i];
+            s = fmaf(v, v, s);
+            nf |= !isfinite(v);
+        }
+        ss += (double)s;
+    }
+    __device__ __forceinline__ void add1(float x, bool f16) {
+        const float v = f16 ? __half2float(__float2half_rn(x)) : x;
+        ss += (double)v * (double)v;
+        nf |= !isfinite(v);
+    }
+    // warp-collective: every lane of the warp must call it
+    __device__ __forceinline__ void flush(double *sumsq, int32_t *nonfinite, int tensor) {
+        double v = ss;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        const unsigned anynf = __reduce_or_sync(0xffffffffu, nf);
+        if ((threadIdx.x & 31) == 0) {
+            if (v != 0.0) atomicAdd(sumsq + tensor, v);
+            if (anynf) atomicOr(nonfinite, 1);
+        }
+        ss = 0.0;
+        nf = 0;
+    }
+};
+
 __device__ __forceinline__ void grad_store1(char *g, int64_t idx, bool f16, float x) {
     if (f16) *reinterpret_cast<__half *>(g + idx * 2) = __float2half_rn(x);
     else *reinterpret_cast<float *>(g + idx * 4) = x;
@@ -483,7 +519,7 @@ constexpr int LC_THREADS = 256;
 constexpr int LC_SUBS = 8;     // warp sub-items per chunk
 constexpr int LC_UNROLL = 4;
 
-template <typename BT>
+template <typename BT, bool STATS>
 __global__ void __launch_bounds__(LC_THREADS, 3) local_kernel(DataParams p) {
     using B = Buf<BT>;
     const int lane = threadIdx.x & 31;
@@ -507,6 +543,7 @@ __global__ void __launch_bounds__(LC_THREADS, 3) local_kernel(DataParams p) {
             if (lo >= hi) continue;
             char *g = reinterpret_cast<char *>(p.dev_ptr[sg.tensor]);
             const bool f16 = sg.grad_f16 != 0;
+            GradStat gs;
             const int64_t toff = sg.tensor_off + (lo - sg.buf_off);
             const bool aligned = ((reinterpret_cast<uintptr_t>(g) + toff * (f16 ? 2 : 4)) & 15) == 0;
             const int64_t n = hi - lo;
@@ -527,12 +564,15 @@ __global__ void __launch_bounds__(LC_THREADS, 3) local_kernel(DataParams p) {
                     for (int i = 0; i < 8; ++i) x[i] = x[i] * p.inv_n;  // sum of one rank, x 1/N
                     B::from_f32(x);                                   // fl_b(. * 1/N)
                     grad_store(g, toff + 8 * v, f16, x);              // unpack: fl_g
+                    if (STATS) gs.add8(x, f16);
                 }
             }
             for (int64_t e = nvec * 8 + lane; e < n; e += 32) {
                 const float y = B::round1(B::round1(grad_load1(g, toff + e, f16)) * p.inv_n);
                 grad_store1(g, toff + e, f16, y);
+                if (STATS) gs.add1(y, f16);
             }
+            if (STATS) gs.flush(p.sumsq, p.nonfinite, sg.tensor);
         }
     }
 }
@@ -603,10 +643,12 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t *b, uint32_t tx) {
 // One gradient piece = the overlap of a segment of chunk c with the sub-tile [sb, se).
 struct Piece {
     char *g;          // gradient tensor base
+    int32_t tensor;   // tensor id
     int64_t lo, n;    // fusion-buffer index of the first element, element count
     int64_t toff;     // tensor index of the first element
     int64_t body;     // leading elements staged in shared memory by TMA (0: none)
     bool f16;
+    bool galigned;    // gradient address 16-byte aligned (vector stores possible)
 };
 
 constexpr int XF_MAXP = 8;  // gradient pieces described in a stage's metadata (more: slow path)
@@ -622,12 +664,14 @@ __device__ __forceinline__ bool piece_of(const DataParams &p, const Seg &sg, int
     const int64_t hi = (sg.buf_off + sg.len) < se ? (sg.buf_off + sg.len) : se;
     if (lo >= hi) return false;
     pc.g = reinterpret_cast<char *>(p.dev_ptr[sg.tensor]);
+    pc.tensor = sg.tensor;
     pc.f16 = sg.grad_f16 != 0;
     pc.lo = lo;
     pc.n = hi - lo;
     pc.toff = sg.tensor_off + (lo - sg.buf_off);
     const int64_t esz = pc.f16 ? 2 : 4;
     const bool aligned = ((reinterpret_cast<uintptr_t>(pc.g) + pc.toff * esz) & 15) == 0;
+    pc.galigned = aligned;
     pc.body = aligned ? ((pc.n * esz) & ~(int64_t)15) / esz : 0;
     return true;
 }
@@ -645,7 +689,7 @@ __device__ __forceinline__ float lds_grad1(const char *src, int64_t e, bool f16)
 
 // Consumers: one staged sub-tile [sb, se) of chunk c. Peer copies sit in slots 0..N-2 of
 // the stage (slot_bytes apart), own gradient pieces in the gradient slot (PACK/RED/RS).
-template <typename BT, int KIND>
+template <typename BT, int KIND, bool STATS>
 __device__ __forceinline__ void xf_consume(const DataParams &p, const XfMeta &m, const char *stage,
                                            int64_t slot_bytes, const char *gslot, int ct, char *own_buf) {
     using B = Buf<BT>;
@@ -662,7 +706,11 @@ __device__ __forceinline__ void xf_consume(const DataParams &p, const XfMeta &m,
         }
         const int64_t esz = pc.f16 ? 2 : 4;
         const char *gs = gslot + (pc.lo - sb) * 4;  // staged own gradient piece
-        const int64_t nvec = pc.body >> 3;
+        // vectors: the staged body for kinds that read the own gradient; for AG (reads only the
+        // peer slot) every whole vector of an aligned gradient — the same split as the RS path
+        // (body = n rounded down to 16 B), so statistics group elements identically on all ranks
+        const int64_t nvec = (KIND == K_AG) ? (pc.galigned ? (pc.n >> 3) : 0) : (pc.body >> 3);
+        GradStat st;
         for (int64_t v = ct; v < nvec; v += XF_CONS) {
             const int64_t e = 8 * v, bi = pc.lo + e, ti = pc.toff + e;
             const int64_t so = (bi - sb) * B::ES;  // byte offset inside a peer slot
@@ -695,6 +743,7 @@ __device__ __forceinline__ void xf_consume(const DataParams &p, const XfMeta &m,
                 if constexpr (KIND == K_RS) B::store(own_buf, bi, out);
             }
             grad_store(pc.g, ti, pc.f16, acc);
+            if (STATS) st.add8(acc, pc.f16);
         }
         for (int64_t e = nvec * 8 + ct; e < pc.n; e += XF_CONS) {  // remainder, tail, unaligned
             const int64_t bi = pc.lo + e, ti = pc.toff + e;
@@ -720,7 +769,9 @@ __device__ __forceinline__ void xf_consume(const DataParams &p, const XfMeta &m,
                 if constexpr (KIND == K_RS) B::store1(own_buf, bi, y);
             }
             grad_store1(pc.g, ti, pc.f16, y);
+            if (STATS) st.add1(y, pc.f16);
         }
+        if (KIND != K_PACK && STATS) st.flush(p.sumsq, p.nonfinite, pc.tensor);
     }
 }
 
@@ -728,7 +779,7 @@ __device__ __forceinline__ void xf_consume(const DataParams &p, const XfMeta &m,
 // broadcast the result into every rank's copy, and unpack it into this rank's gradients.
 // Works on whole 8-element buffer vectors (tensor starts are 8-aligned in the layout, so a
 // tail vector only covers padding beyond the tensor); gradients get only valid elements.
-template <typename BT>
+template <typename BT, bool STATS>
 __device__ __forceinline__ void xf_nvls_reduce(const DataParams &p, const XfMeta &m, int ct) {
     using B = Buf<BT>;
     BT *mc = reinterpret_cast<BT *>(p.nvls_mc);
@@ -744,6 +795,7 @@ __device__ __forceinline__ void xf_nvls_reduce(const DataParams &p, const XfMeta
         const int64_t esz = pc.f16 ? 2 : 4;
         const bool galigned = ((reinterpret_cast<uintptr_t>(pc.g) + pc.toff * esz) & 15) == 0;
         const int64_t nv = (pc.n + 7) >> 3;  // buffer vectors (the last may cover padding)
+        GradStat st;
         constexpr int U = 4;                 // switch reductions in flight per thread
         for (int64_t v0 = ct; v0 < nv; v0 += (int64_t)XF_CONS * U) {
             float x[U][8];
@@ -765,11 +817,16 @@ __device__ __forceinline__ void xf_nvls_reduce(const DataParams &p, const XfMeta
                 const int64_t e = 8 * v;
                 if (galigned && e + 8 <= pc.n) {
                     grad_store(pc.g, pc.toff + e, pc.f16, x[u]);
+                    if (STATS) st.add8(x[u], pc.f16);
                 } else {
-                    for (int i = 0; i < 8 && e + i < pc.n; ++i) grad_store1(pc.g, pc.toff + e + i, pc.f16, x[u][i]);
+                    for (int i = 0; i < 8 && e + i < pc.n; ++i) {
+                        grad_store1(pc.g, pc.toff + e + i, pc.f16, x[u][i]);
+                        if (STATS) st.add1(x[u][i], pc.f16);
+                    }
                 }
             }
         }
+        if (STATS) st.flush(p.sumsq, p.nonfinite, pc.tensor);
     }
 }
 
@@ -778,7 +835,7 @@ constexpr int XF_RCACHE = 512;  // released groups cached in shared memory for i
 // 96 registers x 512 threads leaves room on every SM for a concurrently running
 // bitvector kernel (256 threads), so the next cycle's coordination never queues behind
 // a long reduction.
-template <typename BT>
+template <typename BT, bool STATS>
 __global__ void __maxnreg__(96) xfer_kernel(DataParams p) {
     using B = Buf<BT>;
     extern __shared__ __align__(1024) char xsm[];
@@ -855,12 +912,14 @@ __global__ void __maxnreg__(96) xfer_kernel(DataParams p) {
                     if (lo < hi) {
                         has = true;
                         pc.g = gp;
+                        pc.tensor = sg.tensor;
                         pc.f16 = sg.grad_f16 != 0;
                         pc.lo = lo;
                         pc.n = hi - lo;
                         pc.toff = sg.tensor_off + (lo - sg.buf_off);
                         const int64_t esz = pc.f16 ? 2 : 4;
                         const bool al = ((reinterpret_cast<uintptr_t>(gp) + pc.toff * esz) & 15) == 0;
+                        pc.galigned = al;
                         pc.body = al ? ((pc.n * esz) & ~(int64_t)15) / esz : 0;
                     }
                 }
@@ -977,11 +1036,11 @@ __global__ void __maxnreg__(96) xfer_kernel(DataParams p) {
             const int item = m.item, c = m.chunk, last = m.last;
             const char *st = xsm + (size_t)stage * stage_bytes;
             char *own = ALGO == ALGO_NVLS ? p.nvls_uc : p.buf[p.rank];  // this rank's fusion buffer
-            if (kind == K_PACK) xf_consume<BT, K_PACK>(p, m, st, 0, st, ct, own);
-            else if (kind == K_RED) xf_consume<BT, K_RED>(p, m, st, p.slot_bytes_red, st + gslot_off, ct, own);
-            else if (kind == K_RS) xf_consume<BT, K_RS>(p, m, st, p.slot_bytes_red, st + gslot_off, ct, own);
-            else if (kind == K_NRS) xf_nvls_reduce<BT>(p, m, ct);
-            else xf_consume<BT, K_AG>(p, m, st, 0, st, ct, own);
+            if (kind == K_PACK) xf_consume<BT, K_PACK, STATS>(p, m, st, 0, st, ct, own);
+            else if (kind == K_RED) xf_consume<BT, K_RED, STATS>(p, m, st, p.slot_bytes_red, st + gslot_off, ct, own);
+            else if (kind == K_RS) xf_consume<BT, K_RS, STATS>(p, m, st, p.slot_bytes_red, st + gslot_off, ct, own);
+            else if (kind == K_NRS) xf_nvls_reduce<BT, STATS>(p, m, ct);
+            else xf_consume<BT, K_AG, STATS>(p, m, st, 0, st, ct, own);
             // the stage is free once every consumer warp has read it
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[stage]);
@@ -1019,27 +1078,28 @@ __global__ void __maxnreg__(96) xfer_kernel(DataParams p) {
     }
 }
 
-template <typename BT>
+template <typename BT, bool STATS>
 static int launch_data_t(const DataParams &p, int local, int ctas, cudaStream_t s) {
     static bool attr_set = false;
     if (!attr_set) {
-        cudaFuncSetAttribute(xfer_kernel<BT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 208 * 1024);
+        cudaFuncSetAttribute(xfer_kernel<BT, STATS>, cudaFuncAttributeMaxDynamicSharedMemorySize, 208 * 1024);
         attr_set = true;
     }
-    if (local) local_kernel<BT><<<ctas, LC_THREADS, 0, s>>>(p);
-    else xfer_kernel<BT><<<ctas, XF_THREADS, (size_t)p.nstages * p.stage_bytes, s>>>(p);
+    if (local) local_kernel<BT, STATS><<<ctas, LC_THREADS, 0, s>>>(p);
+    else xfer_kernel<BT, STATS><<<ctas, XF_THREADS, (size_t)p.nstages * p.stage_bytes, s>>>(p);
     return (int)cudaGetLastError();
 }
 
 int launch_data(const DataParams &p, int local, int buffer_f16, int ctas, void *stream) {
     cudaStream_t s = (cudaStream_t)stream;
-    return buffer_f16 ? launch_data_t<__half>(p, local, ctas, s) : launch_data_t<float>(p, local, ctas, s);
+    if (p.sumsq) return buffer_f16 ? launch_data_t<__half, true>(p, local, ctas, s) : launch_data_t<float, true>(p, local, ctas, s);
+    return buffer_f16 ? launch_data_t<__half, false>(p, local, ctas, s) : launch_data_t<float, false>(p, local, ctas, s);
 }
 
 template <typename BT>
 static int max_ctas_t(int *out) {
     int per_sm = 0, dev = 0, sms = 0;
-    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, local_kernel<BT>, LC_THREADS, 0);
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, local_kernel<BT, false>, LC_THREADS, 0);
     if (e != cudaSuccess) return (int)e;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);

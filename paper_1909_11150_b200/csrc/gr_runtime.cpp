@@ -126,6 +126,11 @@ struct gr_ctx {
     int last_algo = GR_ALGO_NONE;
     std::string err = "no error";
 
+    // NEXT-2 gradient statistics (optional)
+    double *d_sumsq = nullptr;
+    int32_t *d_nonfinite = nullptr;
+    bool stats_on = false;
+
     // NVLS multicast fusion buffer (optional; see gr_nvls.cpp)
     gr::Nvls nvls;
     std::string nvls_why = "not attempted";
@@ -460,7 +465,7 @@ void free_all(gr_ctx *c) {
     cudaFree(c->symm);
     void *dptrs[] = {c->d_segs, c->d_chunks, c->d_cbeg, c->d_cend, c->d_gbb, c->d_gbe, c->d_gnch, c->d_gcb,
                      c->d_gel, c->d_big, c->d_relw, c->d_hbits_dev, c->d_ptr, c->d_rel_ring, c->d_cum_ring, c->d_info_ring, c->d_counters,
-                     c->d_flags, c->d_trace};
+                     c->d_flags, c->d_trace, c->d_sumsq, c->d_nonfinite};
     for (void *p : dptrs) cudaFree(p);
     cudaFreeHost(c->h_bits);
     cudaFreeHost(c->h_ptr);
@@ -800,6 +805,14 @@ int gr_step(gr_ctx *c, int32_t *released, gr_cycle_info *info, uint32_t *global_
             CK(c, cudaMemcpyAsync(c->d_ptr, c->h_ptr, sizeof(uint64_t) * c->T, cudaMemcpyHostToDevice, c->s_data));
         }
         if (d.trace) CK(c, cudaMemsetAsync(d.trace, 0, sizeof(uint64_t) * c->trace_slot_u64, c->s_data));
+        if (c->stats_on) {
+            d.sumsq = c->d_sumsq;
+            d.nonfinite = c->d_nonfinite;
+            if (step_fresh) {  // statistics restart with the step
+                CK(c, cudaMemsetAsync(c->d_sumsq, 0, sizeof(double) * c->T, c->s_data));
+                CK(c, cudaMemsetAsync(c->d_nonfinite, 0, sizeof(int32_t), c->s_data));
+            }
+        }
         lrc = gr::launch_data(d, local, c->buf_f16, ctas, c->s_data);
         if (lrc) return fail(c, GR_ECUDA, "data launch: %s", cudaGetErrorString((cudaError_t)lrc));
         if (c->timing) {
@@ -998,6 +1011,34 @@ int gr_query(gr_ctx *c, int32_t kind, void *out, size_t bytes) {
         }
         default: return fail(c, GR_EINVAL, "unknown query %d", kind);
     }
+}
+
+int gr_enable_grad_stats(gr_ctx *c, int32_t on) {
+    if (!c) return GR_EINVAL;
+    if (c->dry) return fail(c, GR_ESTATE, "dry context (device < 0) has no statistics");
+    if (on && !c->d_sumsq) {
+        CK(c, cudaSetDevice(c->dev));
+        CK(c, cudaMalloc((void **)&c->d_sumsq, sizeof(double) * c->T));
+        CK(c, cudaMalloc((void **)&c->d_nonfinite, sizeof(int32_t)));
+        CK(c, cudaMemset(c->d_sumsq, 0, sizeof(double) * c->T));
+        CK(c, cudaMemset(c->d_nonfinite, 0, sizeof(int32_t)));
+    }
+    c->stats_on = on != 0;
+    return GR_OK;
+}
+
+int gr_grad_stats(gr_ctx *c, double *sumsq_host, int32_t *nonfinite_host, void **sumsq_dev, void **nonfinite_dev) {
+    if (!c) return GR_EINVAL;
+    if (!c->stats_on || !c->d_sumsq) return fail(c, GR_ESTATE, "gradient statistics are not enabled");
+    if (sumsq_dev) *sumsq_dev = c->d_sumsq;
+    if (nonfinite_dev) *nonfinite_dev = c->d_nonfinite;
+    if (sumsq_host || nonfinite_host) {
+        CK(c, cudaSetDevice(c->dev));
+        CK(c, cudaStreamSynchronize(c->s_data));
+        if (sumsq_host) CK(c, cudaMemcpy(sumsq_host, c->d_sumsq, sizeof(double) * c->T, cudaMemcpyDeviceToHost));
+        if (nonfinite_host) CK(c, cudaMemcpy(nonfinite_host, c->d_nonfinite, sizeof(int32_t), cudaMemcpyDeviceToHost));
+    }
+    return GR_OK;
 }
 
 int gr_set_timing(gr_ctx *c, int32_t on) {

@@ -32,7 +32,7 @@ def main():
 
     from paper_1909_11150_b200 import GR_F16, GR_F32, Context, make_allgather
     from paper_1909_11150_b200.binding import GR_Q_NVLS
-    from tests.parity_lib import run_case_on_rank
+    from tests.parity_lib import check_grad_stats, run_case_on_rank
     from workloads import cfg1_case, fcn220m
     from workloads.schedules import Case, random_mark_schedule, random_partition, reverse_layer_schedule
 
@@ -47,13 +47,15 @@ def main():
     failures = 0
     ncase = 0
 
-    def run(case, seed, buf, grad_f16=None, kind="uniform", chunk=0, osm=None, max_cycles=None):
+    def run(case, seed, buf, grad_f16=None, kind="uniform", chunk=0, osm=None, max_cycles=None, stats=False):
         nonlocal failures, ncase
         ncase += 1
         ctx = Context(rank=rank, world_size=N, device=local, numel=case.numel, group_of=case.group_of,
                       grad_f16=grad_f16, buffer_dtype=GR_F16 if buf == "f16" else GR_F32,
                       one_shot_max_bytes=args.one_shot_max_bytes if osm is None else osm,
                       chunk_elems=chunk or args.chunk_elems, timeout_ms=20000, allgather=ag)
+        if stats:
+            ctx.gr_enable_grad_stats(True)
         ok = True
         nvls, why = ctx.nvls()
         if os.environ.get("GR_NVLS") == "1" and not nvls:
@@ -61,6 +63,15 @@ def main():
         try:
             _log, h = run_case_on_rank(ctx, case, rank, seed, dev, buf == "f16", grad_f16, kind,
                                        max_cycles=max_cycles, exact=not nvls)
+            if stats:
+                ss = check_grad_stats(ctx, case, seed, buf == "f16", grad_f16, kind, exact=not nvls,
+                                      where=f"rank {rank} seed {seed}")
+                all_ss = [None] * N
+                dist.all_gather_object(all_ss, ss)
+                for other in all_ss:  # fp64 atomics: equal up to summation order (~1e-15)
+                    for a, b in zip(ss, other):
+                        assert abs(a - b) <= 1e-12 * max(abs(a), abs(b)) + 1e-300, \
+                            f"rank {rank} seed {seed}: statistics differ across ranks {a!r} {b!r}"
         except AssertionError as e:
             ok = False
             h = "FAIL"
@@ -92,6 +103,16 @@ def main():
                     for osm in (0, 1 << 62):  # force two-shot, force one-shot
                         run(case, seed, buf, grad_f16=gf, chunk=int(rng.choice([1024, 4096, 32768])), osm=osm)
                     run(case, seed, buf, kind="int", osm=0)
+            elif args.suite == "stats":
+                for seed in range(s0, s1):
+                    rng = np.random.default_rng(seed + 77)
+                    T = int(rng.integers(2, 20))
+                    numel = rng.integers(1, 300000, size=T).astype(np.int64)
+                    case = Case(N, numel, random_partition(T, int(rng.integers(1, T + 1)), rng),
+                                random_mark_schedule(N, T, seed, 3), seed)
+                    gf = (rng.random(T) < 0.3).tolist()
+                    for osm in (0, 1 << 62):
+                        run(case, seed, buf, grad_f16=gf, osm=osm, stats=True)
             elif args.suite == "fcn":
                 f = fcn220m()
                 mark = reverse_layer_schedule(len(f.layers), N, f.release_order, layers_per_cycle=1,

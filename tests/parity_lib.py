@@ -103,3 +103,22 @@ def run_case_on_rank(ctx, case, r, seed, device, buffer_f16: bool, grad_f16=None
         check_values(out[idx], gs, case.N, buffer_f16, f16, where=f"rank {r} seed {seed} tensor {t}",
                      exact=exact or kind == "int")
     return log, h.hexdigest()
+
+
+def check_grad_stats(ctx, case, seed, buffer_f16: bool, grad_f16=None, kind="uniform", exact: bool = True,
+                     where=""):
+    """NEXT-2 epilogue: per-tensor sum of squares of the reduced gradient against the fp64 sum of
+    squares of the oracle's emulated values (relative 1e-6: the kernels sum fp32 squares of 8
+    values before the fp64 accumulation), and the non-finite flag (False for finite inputs)."""
+    sumsq, nonfinite = ctx.gr_grad_stats()
+    assert not nonfinite, f"{where}: non-finite flag set on finite inputs"
+    for t in range(case.T):
+        f16 = bool(grad_f16 is not None and grad_f16[t])
+        gs = host_inputs(case.numel, case.N, seed, t, f16, kind)
+        emu = oracle.emulate(gs, buffer_f16, f16).astype(np.float64)
+        want = float(np.sum(emu * emu))
+        tol = 1e-6 * want + 1e-30
+        if not exact:  # NVLS: values within the north-star tolerance, so compare loosely
+            tol = 2.0 ** -9 * want + 1e-30
+        assert abs(sumsq[t] - want) <= tol, f"{where}: tensor {t} sumsq gpu={sumsq[t]!r} oracle={want!r}"
+    return sumsq

@@ -154,6 +154,35 @@ def test_async_wait_pipelined_steps(gpu):
     ctx.gr_finalize()
 
 
+@pytest.mark.parametrize("buf16", [True, False])
+def test_grad_stats_epilogue_n1(gpu, buf16):
+    """NEXT-2: fused ||g||^2 per tensor and non-finite flag, checked against the oracle."""
+    import math
+    from tests.parity_lib import check_grad_stats, run_case_on_rank
+    from harness.replay import make_grads
+    rng = np.random.default_rng(5)
+    T = 12
+    numel = rng.integers(1, 200000, size=T).astype(np.int64)
+    case = Case(1, numel, random_partition(T, 4, rng), random_mark_schedule(1, T, 5, 2), 5)
+    gf = (rng.random(T) < 0.3).tolist()
+    ctx = _ctx(case, buf16, grad_f16=gf)
+    ctx.gr_enable_grad_stats(True)
+    run_case_on_rank(ctx, case, 0, 5, gpu, buf16, grad_f16=gf)
+    check_grad_stats(ctx, case, 5, buf16, grad_f16=gf)
+    # a step with an Inf in tensor 3: flag set, that tensor's norm is Inf, the others finite
+    grads = make_grads(case.numel, 0, 5, gpu, gf)
+    grads[3].view(-1)[min(7, grads[3].numel() - 1)] = float("inf")
+    ctx.gr_mark_ready_batch(list(range(T)), [g.data_ptr() for g in grads])
+    while True:
+        _rel, complete, _, _ = ctx.gr_step()
+        if complete:
+            break
+    ctx.gr_wait()
+    sumsq, nonfinite = ctx.gr_grad_stats()
+    assert nonfinite and math.isinf(sumsq[3]) and all(math.isfinite(v) for i, v in enumerate(sumsq) if i != 3)
+    ctx.gr_finalize()
+
+
 def test_async_marks_follow_stream(gpu):
     """gr_mark_ready_async: the flag lands only after the stream's prior work."""
     import torch
@@ -228,3 +257,12 @@ def test_multi_gpu_nvls(n):
         pytest.skip(f"needs {n} GPUs")
     assert _torchrun(n, "--suite", "edge", "--seeds", "0:3", env_extra={"GR_NVLS": "1"}) == 0
     assert _torchrun(n, "--suite", "fcn", "--seeds", "7:8", env_extra={"GR_NVLS": "1"}) == 0
+
+
+@pytest.mark.parametrize("n", [2, 4, 8])
+def test_multi_gpu_grad_stats(n):
+    """NEXT-2 epilogue at N ranks: every rank's per-tensor ||g||^2 matches the oracle and the
+    other ranks' (every rank holds the full reduced gradient)."""
+    if gpu_count() < n:
+        pytest.skip(f"needs {n} GPUs")
+    assert _torchrun(n, "--suite", "stats", "--seeds", "0:3") == 0
