@@ -34,7 +34,7 @@ namespace {
 
 thread_local std::string g_init_error = "no error";
 
-constexpr int64_t kDefaultChunkElems = 32768;
+constexpr int64_t kMaxChunkElems = 131072;  // largest adaptive chunk (elements)
 constexpr int32_t kDefaultTimeoutMs = 20000;
 constexpr size_t kAlign = 256;
 
@@ -58,7 +58,7 @@ struct gr_ctx {
     int32_t T = 0, G = 0, W = 0, nbits = 0, N = 1, rank = 0;
     bool dry = false;
     int buf_f16 = 1;
-    int64_t chunk_elems = kDefaultChunkElems;
+    int64_t chunk_elems = 0;  // 0 = adaptive per group
     int64_t one_shot_max_bytes = 0;
     uint64_t hash = 0;
 
@@ -108,7 +108,7 @@ struct gr_ctx {
     PFN_writeValue32 write_value32 = nullptr;
     int data_ctas[4] = {0, 0, 0, 0};
     int lag1 = 0, lag2 = 0;  // GR_LAG1 / GR_LAG2 overrides (tuning)
-    int nstages = 6, stage_kb = 32;  // GR_STAGES / GR_STAGE_KB overrides (tuning)
+    int nstages = 4, stage_kb = 48;  // GR_STAGES / GR_STAGE_KB overrides (tuning)
 
     // step / cycle state
     std::mutex mu;
@@ -258,8 +258,17 @@ int build_layouts(gr_ctx *c, const gr_tensor *table, const int32_t *group_of) {
         c->gchunk_begin[g] = (int32_t)c->chunks.size();
         const int32_t pos0 = pos;
         while (pos < T && group_of[order[pos]] == g) ++pos;
-        for (int64_t cb = gbeg[g]; cb < gend[g]; cb += c->chunk_elems) {
-            const int64_t ce = std::min(gend[g], cb + c->chunk_elems);
+        // chunk size: fixed when the caller asks for one; otherwise per group, about two chunks
+        // per SM for the group alone (power of two in [8K, 128K] elements): large groups get
+        // large items (fewer flags, longer TMA streams), small ones keep every SM busy
+        int64_t cg = c->chunk_elems;
+        if (cg == 0) {
+            const int64_t target = std::max<int64_t>(1, (gend[g] - gbeg[g]) / 296);
+            cg = 8192;
+            while (cg * 2 <= target && cg < 131072) cg *= 2;
+        }
+        for (int64_t cb = gbeg[g]; cb < gend[g]; cb += cg) {
+            const int64_t ce = std::min(gend[g], cb + cg);
             Chunk ch;
             ch.seg_begin = (int32_t)c->segs.size();
             for (int32_t q = pos0; q < pos; ++q) {
@@ -536,7 +545,9 @@ int gr_init(gr_ctx **out, const gr_world *world, const gr_tensor *table, int32_t
     c->N = world->world_size;
     c->rank = world->rank;
     c->buf_f16 = world->buffer_dtype == GR_F16;
-    c->chunk_elems = world->chunk_elems > 0 ? world->chunk_elems : kDefaultChunkElems;
+    c->chunk_elems = world->chunk_elems;  // 0: adaptive per group (build_layouts)
+    if (world->chunk_elems == 0)
+        if (const char *ce = getenv("GR_CHUNK_ELEMS")) c->chunk_elems = std::max<int64_t>(8, atoll(ce) / 8 * 8);  // tuning
     // default one-shot threshold: at N=2 one-shot moves the same NVLink bytes as two-shot
     // with one fewer synchronisation, so it is used at every size; above N=2 it is kept for
     // latency-bound messages.
@@ -778,11 +789,12 @@ int gr_step(gr_ctx *c, int32_t *released, gr_cycle_info *info, uint32_t *global_
         d.nstages = c->nstages;
         // RED/RS stage: N-1 peer slots (buffer precision) + one fp32-spaced gradient slot
         int64_t sr = c->N > 1 ? stage / ((c->N - 1) * es + 4) / 256 * 256 : 256;
-        sr = std::max<int64_t>(256, std::min<int64_t>(sr, c->chunk_elems));
+        const int64_t cmax = c->chunk_elems > 0 ? c->chunk_elems : kMaxChunkElems;
+        sr = std::max<int64_t>(256, std::min<int64_t>(sr, cmax));
         d.sub_red = sr;
         d.slot_bytes_red = sr * es;
-        d.sub_pack = std::max<int64_t>(256, std::min<int64_t>(stage / 4 / 256 * 256, c->chunk_elems));
-        d.sub_ag = std::max<int64_t>(256, std::min<int64_t>(stage / es / 256 * 256, c->chunk_elems));
+        d.sub_pack = std::max<int64_t>(256, std::min<int64_t>(stage / 4 / 256 * 256, cmax));
+        d.sub_ag = std::max<int64_t>(256, std::min<int64_t>(stage / es / 256 * 256, cmax));
         d.one_shot_max_bytes = c->one_shot_max_bytes;
         d.rank = c->rank;
         d.N = c->N;
