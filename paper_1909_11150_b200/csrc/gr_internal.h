@@ -50,6 +50,8 @@ struct DevCycle {
     int32_t n_released;
     int32_t total_chunks;
     int64_t elems;
+    int32_t total_subs;    // local-kernel sub-items of the released groups
+    int32_t pad;
 };
 
 struct BvParams {
@@ -62,6 +64,7 @@ struct BvParams {
     const int32_t *group_bit_begin;  // device [G]
     const int32_t *group_bit_end;    // device [G]
     const int32_t *group_nchunks;    // device [G]
+    const int32_t *group_nsub;       // device [G]: local-kernel sub-items of the group
     const int64_t *group_elems;      // device [G]
     const int32_t *big_groups;       // device [n_big]: groups spanning > 8 bitvector words
     int32_t n_big;
@@ -69,6 +72,7 @@ struct BvParams {
     int32_t *out_released;           // device [G]   (ring slot)
     int32_t *out_cum;                // device [G+1] (ring slot)
     DevCycle *out_info;              // device (ring slot)
+    int32_t *out_subcum;             // device [G+1] (ring slot): prefix of group_nsub over the list
     HostResult *result;              // host-mapped
     int32_t T, G, W, nbits, rank, N;
     uint32_t epoch;                  // training-step epoch (>= 1)
@@ -90,6 +94,8 @@ struct DataParams {
     const int32_t *released;           // ring slot [G]
     const int32_t *cum;                // ring slot [G+1]
     const DevCycle *info;              // ring slot: released groups / chunks / elements
+    const int32_t *subcum;             // ring slot [G+1]: local-kernel sub-item prefix
+    const int32_t *group_spc;          // [G]: local-kernel sub-items per full chunk of the group
     const uint64_t *dev_ptr;           // [T]
     char *buf[GR_MAX_RANKS];           // every rank's fusion buffer for this step parity
     char *nvls_uc;                     // NVLS: this rank's copy of the multicast buffer (parity), or null
@@ -100,7 +106,9 @@ struct DataParams {
     int32_t *done_counter;
     volatile int32_t *abort_dev;       // device flag: bail out (set on timeout)
     HostError *err;                    // host-mapped
-    uint64_t *trace;                   // optional [items][4]: grab, ready, done, cta|smid<<32
+    uint64_t *trace;                   // optional [items][4]: grab, ready, done, cta|smid<<32, then
+                                       // per CTA 8 u64 of stall counters (xfer kernel)
+    int32_t trace_items;               // item slots in the trace before the per-CTA counters (= C)
     const int64_t *chunk_begin;        // [C] fusion-buffer element range of each chunk
     const int64_t *chunk_end;          // [C]
     int64_t stage_bytes;               // xfer kernel: bytes of one shared-memory stage
@@ -108,6 +116,7 @@ struct DataParams {
     int64_t slot_bytes_red;            // bytes of one peer's slot inside a stage
     int64_t sub_red, sub_ag, sub_pack; // staged sub-tile (elements) for reduce / all-gather / pack items
     int32_t lag1, lag2;                // queue lags (in released chunks) of reduce / all-gather items
+    int64_t lc_sub;                    // local kernel: elements per warp sub-item (multiple of 8)
     int64_t one_shot_max_bytes;        // N>1: messages up to this many buffer bytes go one-shot
     double *sumsq;                     // optional [T]: sum of squares of the reduced gradient (NEXT-2)
     int32_t *nonfinite;                // optional: set to 1 if any reduced value is Inf/NaN

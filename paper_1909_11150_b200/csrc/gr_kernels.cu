@@ -81,10 +81,10 @@ __global__ void __launch_bounds__(BV_THREADS, 4) bitvector_kernel(BvParams p) {
     const int W = p.W, G = p.G, Gw = (p.G + 31) / 32;
     uint32_t *sL = smem, *sA = smem + W, *sR = smem + 2 * W, *sC = smem + 3 * W;
     __shared__ int s_timeout;
-    __shared__ int s_scan[BV_THREADS / 32][2];
+    __shared__ int s_scan[BV_THREADS / 32][3];
     __shared__ unsigned long long s_elems;
     __shared__ int s_all[BV_THREADS / 32];
-    __shared__ int s_tot[2];
+    __shared__ int s_tot[3];
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
     const uint64_t t_start = globaltimer();
@@ -192,57 +192,68 @@ __global__ void __launch_bounds__(BV_THREADS, 4) bitvector_kernel(BvParams p) {
     // of (count, chunks) gives every released group its slot in the ascending list and its
     // chunk prefix; the group's bits join the released set.
     const int per = (Gw + blockDim.x - 1) / blockDim.x;
-    int my_cnt = 0, my_ch = 0;
+    int my_cnt = 0, my_ch = 0, my_sub = 0;
     long long my_el = 0;
     for (int i = tid * per; i < min(Gw, (tid + 1) * per); ++i)
         for (uint32_t m = sC[i]; m; m &= m - 1) {
             const int g = i * 32 + __ffs(m) - 1;
             ++my_cnt;
             my_ch += p.group_nchunks[g];
+            my_sub += p.group_nsub[g];
             my_el += p.group_elems[g];
         }
-    int xc = my_cnt, xh = my_ch;  // inclusive warp scans
+    int xc = my_cnt, xh = my_ch, xs = my_sub;  // inclusive warp scans
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
         const int yc = __shfl_up_sync(0xffffffffu, xc, o), yh = __shfl_up_sync(0xffffffffu, xh, o);
-        if (lane >= o) { xc += yc; xh += yh; }
+        const int ys = __shfl_up_sync(0xffffffffu, xs, o);
+        if (lane >= o) { xc += yc; xh += yh; xs += ys; }
     }
     long long e = my_el;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) e += __shfl_down_sync(0xffffffffu, e, o);
     if (lane == 0 && e) atomicAdd(&s_elems, (unsigned long long)e);
-    if (lane == 31) { s_scan[warp][0] = xc; s_scan[warp][1] = xh; }
+    if (lane == 31) { s_scan[warp][0] = xc; s_scan[warp][1] = xh; s_scan[warp][2] = xs; }
     __syncthreads();
     if (tid == 0) {
-        int c0 = 0, h0 = 0;
+        int c0 = 0, h0 = 0, s0 = 0;
         for (int i = 0; i < nwarps; ++i) {
-            const int c = s_scan[i][0], h = s_scan[i][1];
+            const int c = s_scan[i][0], h = s_scan[i][1], q = s_scan[i][2];
             s_scan[i][0] = c0;
             s_scan[i][1] = h0;
+            s_scan[i][2] = s0;
             c0 += c;
             h0 += h;
+            s0 += q;
         }
         s_tot[0] = c0;
         s_tot[1] = h0;
+        s_tot[2] = s0;
     }
     __syncthreads();
     int32_t *hrel = reinterpret_cast<int32_t *>(reinterpret_cast<uint32_t *>(p.result + 1) + W);
     {
         int idx = s_scan[warp][0] + xc - my_cnt, ch = s_scan[warp][1] + xh - my_ch;
+        int sbase = s_scan[warp][2] + xs - my_sub;
         for (int i = tid * per; i < min(Gw, (tid + 1) * per); ++i)
             for (uint32_t m = sC[i]; m; m &= m - 1) {
                 const int g = i * 32 + __ffs(m) - 1;
                 p.out_released[idx] = g;
                 p.out_cum[idx] = ch;
+                p.out_subcum[idx] = sbase;
                 hrel[idx] = g;
                 ++idx;
                 ch += p.group_nchunks[g];
+                sbase += p.group_nsub[g];
                 const int b0 = p.group_bit_begin[g], b1 = p.group_bit_end[g];
                 for (int w = b0 >> 5; w <= ((b1 - 1) >> 5); ++w) atomicOr(&sR[w], word_mask(w, b0, b1));
             }
     }
     const int run_base = s_tot[0], run_ch = s_tot[1];
-    if (tid == 0) p.out_cum[run_base] = run_ch;
+    if (tid == 0) {
+        p.out_cum[run_base] = run_ch;
+        p.out_subcum[run_base] = s_tot[2];
+    }
     __syncthreads();
 
     // ---- step_complete: every tensor released in this step ----
@@ -265,6 +276,7 @@ __global__ void __launch_bounds__(BV_THREADS, 4) bitvector_kernel(BvParams p) {
         for (int i = 0; i < nwarps; ++i) complete &= s_all[i];
         p.out_info->n_released = (status == ST_OK) ? run_base : 0;
         p.out_info->total_chunks = (status == ST_OK) ? run_ch : 0;
+        p.out_info->total_subs = (status == ST_OK) ? s_tot[2] : 0;
         p.out_info->elems = (status == ST_OK) ? (int64_t)s_elems : 0;
         p.result->status = status;
         p.result->n_released = run_base;
@@ -516,7 +528,7 @@ __device__ __forceinline__ int chunk_of_item(const DataParams &p, int nrel, int 
 // synchronisation), UNROLL 32-byte vectors in flight per lane, static interleaved schedule.
 // ---------------------------------------------------------------------------------------
 constexpr int LC_THREADS = 256;
-constexpr int LC_SUBS = 8;     // warp sub-items per chunk
+// warp sub-items: p.lc_sub elements each, p.lc_subs slots per chunk
 constexpr int LC_UNROLL = 4;
 
 template <typename BT, bool STATS>
@@ -526,15 +538,22 @@ __global__ void __launch_bounds__(LC_THREADS, 3) local_kernel(DataParams p) {
     const int gw = blockIdx.x * (LC_THREADS / 32) + (threadIdx.x >> 5);
     const int nw = gridDim.x * (LC_THREADS / 32);
     const int nrel = p.info->n_released;
-    const int nitems = p.info->total_chunks * LC_SUBS;
+    const int nitems = p.info->total_subs;
     for (int it = gw; it < nitems; it += nw) {
-        const int c = chunk_of_item(p, nrel, it / LC_SUBS);
-        const int sub = it % LC_SUBS;
+        // sub-item -> released group (prefix over the groups' sub-item counts) -> chunk, offset
+        int lo_ = 0, hi_ = nrel - 1;
+        while (lo_ < hi_) {
+            const int mid = (lo_ + hi_ + 1) >> 1;
+            if (p.subcum[mid] <= it) lo_ = mid; else hi_ = mid - 1;
+        }
+        const int g = p.released[lo_];
+        const int j = it - p.subcum[lo_];
+        const int spc = p.group_spc[g];  // sub-items per full chunk of this group
+        const int c = p.group_chunk_begin[g] + j / spc;
         const int64_t cb = p.chunk_begin[c], ce = p.chunk_end[c];
-        const int64_t len = ((ce - cb + LC_SUBS * 8 - 1) / (LC_SUBS * 8)) * 8;  // multiple of 8
-        const int64_t sb = cb + sub * len;
-        const int64_t se = (sb + len < ce) ? sb + len : ce;
-        if (sb >= se) continue;
+        const int64_t sb = cb + (int64_t)(j % spc) * p.lc_sub;
+        if (sb >= ce) continue;
+        const int64_t se = (sb + p.lc_sub < ce) ? sb + p.lc_sub : ce;
         const Chunk ch = p.chunks[c];
         for (int s = ch.seg_begin; s < ch.seg_end; ++s) {
             const Seg sg = p.segs[s];
@@ -884,6 +903,8 @@ __global__ void __maxnreg__(96) xfer_kernel(DataParams p) {
         int stage = 0;
         uint32_t ph = 1;  // empty barriers start "free"
         const unsigned FULL = 0xffffffffu;
+        long long prof_empty = 0, prof_flags = 0;  // trace mode: producer stall cycles
+        const long long prof_t0 = clock64();
         // stream chunk c as sub-tiles of `sub` elements. src: 0 none (PACK), 1 every peer
         // (RED/RS), 2 the owner (AG); grads: stage own gradient pieces (PACK/RED/RS)
         auto produce = [&](int kind, int item, int c, int64_t sub, int src, int owner, bool grads) {
@@ -900,7 +921,11 @@ __global__ void __maxnreg__(96) xfer_kernel(DataParams p) {
             const int nsub = (int)((ce - cb + sub - 1) / sub);
             for (int t = 0; t < nsub; ++t) {
                 const int64_t sb = cb + t * sub, se = (sb + sub < ce) ? sb + sub : ce;
-                if (lane == 0) mbar_wait(&empty[stage], ph);
+                if (lane == 0) {
+                    const long long t0 = clock64();
+                    mbar_wait(&empty[stage], ph);
+                    prof_empty += clock64() - t0;
+                }
                 __syncwarp();
                 XfMeta &m = meta[stage];
                 char *dst = xsm + (size_t)stage * stage_bytes;
@@ -962,9 +987,12 @@ __global__ void __maxnreg__(96) xfer_kernel(DataParams p) {
         // lane 0: wait for all flags, broadcast the verdict, order the TMA reads after it
         auto wait_flags = [&](const uint32_t *base, int stride, int count, int skip, int where) -> bool {
             int ok = 1;
-            if (lane == 0)
+            if (lane == 0) {
+                const long long t0 = clock64();
                 for (int q = 0; q < count && ok; ++q)
                     if (q != skip) ok = xf_wait_flag(p, base + (size_t)q * stride, where);
+                prof_flags += clock64() - t0;
+            }
             ok = __shfl_sync(FULL, ok, 0);
             asm volatile("fence.proxy.async.global;" ::: "memory");
             return ok != 0;
@@ -1023,13 +1051,25 @@ __global__ void __maxnreg__(96) xfer_kernel(DataParams p) {
             mbar_wait(&empty[stage], ph);
             meta[stage].kind = K_STOP;
             mbar_arrive(&full[stage]);
+            if (p.trace) {  // per-CTA stall profile after the item stamps
+                uint64_t *pr = p.trace + (size_t)3 * p.trace_items + (size_t)blockIdx.x * 8;
+                pr[0] = (uint64_t)(clock64() - prof_t0);
+                pr[1] = (uint64_t)prof_empty;
+                pr[2] = (uint64_t)prof_flags;
+            }
         }
     } else {
         const int ct = tid - 32;  // consumer thread index
         int stage = 0;
         uint32_t ph = 0;
+        long long prof_full = 0, prof_flag = 0;
+        const long long prof_t0 = clock64();
         for (;;) {
-            mbar_wait(&full[stage], ph);
+            {
+                const long long t0 = clock64();
+                mbar_wait(&full[stage], ph);
+                prof_full += clock64() - t0;
+            }
             const XfMeta &m = meta[stage];
             const int kind = m.kind;
             if (kind == K_STOP) break;
@@ -1045,6 +1085,7 @@ __global__ void __maxnreg__(96) xfer_kernel(DataParams p) {
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[stage]);
             if (last && (kind == K_PACK || kind == K_RS || kind == K_NRS)) {  // chunk done: publish its flag
+                const long long t0 = clock64();
                 consumer_sync();
                 if (ct == 0) {
                     fence_sys();
@@ -1057,6 +1098,7 @@ __global__ void __maxnreg__(96) xfer_kernel(DataParams p) {
                         for (int q = 0; q < p.N; ++q) st_relaxed_sys32(p.pack_flag[q] + (size_t)c * p.N + p.rank, p.epoch);
                     }
                 }
+                prof_flag += clock64() - t0;
             }
             if (p.trace && last && ct == 0) {
                 uint32_t smid;
@@ -1065,6 +1107,12 @@ __global__ void __maxnreg__(96) xfer_kernel(DataParams p) {
                 p.trace[(size_t)item * 4 + 3] = (uint64_t)blockIdx.x | ((uint64_t)smid << 32);
             }
             if (++stage == nst) { stage = 0; ph ^= 1; }
+        }
+        if (p.trace && ct == 0) {
+            uint64_t *pr = p.trace + (size_t)3 * p.trace_items + (size_t)blockIdx.x * 8;
+            pr[3] = (uint64_t)(clock64() - prof_t0);
+            pr[4] = (uint64_t)prof_full;
+            pr[5] = (uint64_t)prof_flag;
         }
     }
     __syncthreads();

@@ -65,13 +65,14 @@ struct gr_ctx {
     // host-side layouts
     std::vector<int64_t> numel;
     std::vector<int32_t> grad_f16, group_of, bit_of, tensor_of_bit, group_of_bit;
-    std::vector<int32_t> gbit_begin, gbit_end, gnchunks, gchunk_begin;
+    std::vector<int32_t> gbit_begin, gbit_end, gnchunks, gchunk_begin, gnsub, gspc;
     std::vector<int64_t> buf_off, gelems;
     std::vector<int32_t> big_groups;
     std::vector<Seg> segs;
     std::vector<Chunk> chunks;
     std::vector<int64_t> chunk_begin, chunk_end;
     int64_t buf_elems = 0;
+    int64_t max_chunk = 0;  // longest chunk of the layout (elements)
     int32_t C = 0;
 
     // device state
@@ -87,7 +88,8 @@ struct gr_ctx {
     Seg *d_segs = nullptr;
     Chunk *d_chunks = nullptr;
     int64_t *d_cbeg = nullptr, *d_cend = nullptr;
-    int32_t *d_gbb = nullptr, *d_gbe = nullptr, *d_gnch = nullptr, *d_gcb = nullptr;
+    int32_t *d_gbb = nullptr, *d_gbe = nullptr, *d_gnch = nullptr, *d_gcb = nullptr, *d_gnsub = nullptr,
+            *d_gspc = nullptr, *d_subcum_ring = nullptr;
     int64_t *d_gel = nullptr;
     int32_t *d_big = nullptr;
     uint32_t *d_relw = nullptr, *d_hbits_dev = nullptr;
@@ -109,6 +111,7 @@ struct gr_ctx {
     int data_ctas[4] = {0, 0, 0, 0};
     int lag1 = 0, lag2 = 0;  // GR_LAG1 / GR_LAG2 overrides (tuning)
     int nstages = 4, stage_kb = 48;  // GR_STAGES / GR_STAGE_KB overrides (tuning)
+    int64_t lc_sub = 8192;           // local kernel sub-item (GR_LC_SUB, tuning)
 
     // step / cycle state
     std::mutex mu;
@@ -147,6 +150,7 @@ struct gr_ctx {
         int64_t elems;
     };
     std::vector<TraceCycle> trace_cycles;
+    int64_t trace_written = 0, trace_max = 16;  // GR_TRACE_MAX_CYCLES
 
     // stats / timing
     gr_stats stats{};
@@ -292,6 +296,19 @@ int build_layouts(gr_ctx *c, const gr_tensor *table, const int32_t *group_of) {
         c->gnchunks[g] = (int32_t)c->chunks.size() - c->gchunk_begin[g];
     }
     c->C = (int32_t)c->chunks.size();
+    // local-kernel sub-items (N = 1): lc_sub elements each, spc per full chunk of a group
+    c->gnsub.assign(G, 0);
+    c->gspc.assign(G, 1);
+    for (int32_t g = 0; g < G; ++g) {
+        const int32_t c0 = c->gchunk_begin[g], nc = c->gnchunks[g];
+        const int64_t full = c->chunk_end[c0] - c->chunk_begin[c0];
+        c->gspc[g] = (int32_t)std::max<int64_t>(1, (full + c->lc_sub - 1) / c->lc_sub);
+        const int64_t last = c->chunk_end[c0 + nc - 1] - c->chunk_begin[c0 + nc - 1];
+        c->gnsub[g] = (nc - 1) * c->gspc[g] + (int32_t)((last + c->lc_sub - 1) / c->lc_sub);
+    }
+    c->max_chunk = 0;
+    for (size_t i = 0; i < c->chunks.size(); ++i)
+        c->max_chunk = std::max(c->max_chunk, c->chunk_end[i] - c->chunk_begin[i]);
 
     // hash of everything that must agree across ranks (PAPER.md:108 global consistency)
     uint64_t h = 1469598103934665603ull;
@@ -360,6 +377,8 @@ int setup_device(gr_ctx *c) {
     RC(upload(c, &c->d_gbe, c->gbit_end));
     RC(upload(c, &c->d_gnch, c->gnchunks));
     RC(upload(c, &c->d_gcb, c->gchunk_begin));
+    RC(upload(c, &c->d_gnsub, c->gnsub));
+    RC(upload(c, &c->d_gspc, c->gspc));
     RC(upload(c, &c->d_gel, c->gelems));
     RC(upload(c, &c->d_big, c->big_groups));
     CK(c, cudaMalloc((void **)&c->d_relw, sizeof(uint32_t) * c->W));
@@ -369,6 +388,7 @@ int setup_device(gr_ctx *c) {
     CK(c, cudaMalloc((void **)&c->d_rel_ring, sizeof(int32_t) * GR_SLOT_RING * (size_t)c->G));
     CK(c, cudaMalloc((void **)&c->d_cum_ring, sizeof(int32_t) * GR_SLOT_RING * (size_t)(c->G + 1)));
     CK(c, cudaMalloc((void **)&c->d_info_ring, sizeof(gr::DevCycle) * GR_SLOT_RING));
+    CK(c, cudaMalloc((void **)&c->d_subcum_ring, sizeof(int32_t) * GR_SLOT_RING * (size_t)(c->G + 1)));
     CK(c, cudaMemset(c->d_info_ring, 0, sizeof(gr::DevCycle) * GR_SLOT_RING));
     CK(c, cudaMalloc((void **)&c->d_counters, sizeof(int32_t) * 4));
     CK(c, cudaMemset(c->d_counters, 0, sizeof(int32_t) * 4));
@@ -406,7 +426,8 @@ int setup_device(gr_ctx *c) {
     if (const char *tp = getenv("GR_TRACE")) {
         if (*tp) {
             c->trace_path = std::string(tp) + ".rank" + std::to_string(c->rank) + ".jsonl";
-            c->trace_slot_u64 = (size_t)3 * c->C * 4;
+            if (const char *tm = getenv("GR_TRACE_MAX_CYCLES")) c->trace_max = atoll(tm);
+            c->trace_slot_u64 = (size_t)3 * c->C * 4 + (size_t)1024 * 8;  // items + per-CTA counters
             CK(c, cudaMalloc((void **)&c->d_trace, sizeof(uint64_t) * c->trace_slot_u64 * GR_SLOT_RING));
         }
     }
@@ -473,7 +494,7 @@ void free_all(gr_ctx *c) {
     gr::nvls_free(c->nvls);
     cudaFree(c->symm);
     void *dptrs[] = {c->d_segs, c->d_chunks, c->d_cbeg, c->d_cend, c->d_gbb, c->d_gbe, c->d_gnch, c->d_gcb,
-                     c->d_gel, c->d_big, c->d_relw, c->d_hbits_dev, c->d_ptr, c->d_rel_ring, c->d_cum_ring, c->d_info_ring, c->d_counters,
+                     c->d_gel, c->d_big, c->d_relw, c->d_hbits_dev, c->d_ptr, c->d_rel_ring, c->d_cum_ring, c->d_info_ring, c->d_counters, c->d_gnsub, c->d_gspc, c->d_subcum_ring,
                      c->d_flags, c->d_trace, c->d_sumsq, c->d_nonfinite};
     for (void *p : dptrs) cudaFree(p);
     cudaFreeHost(c->h_bits);
@@ -546,6 +567,7 @@ int gr_init(gr_ctx **out, const gr_world *world, const gr_tensor *table, int32_t
     c->rank = world->rank;
     c->buf_f16 = world->buffer_dtype == GR_F16;
     c->chunk_elems = world->chunk_elems;  // 0: adaptive per group (build_layouts)
+    if (const char *ls = getenv("GR_LC_SUB")) c->lc_sub = std::max<int64_t>(256, atoll(ls) / 8 * 8);  // tuning
     if (world->chunk_elems == 0)
         if (const char *ce = getenv("GR_CHUNK_ELEMS")) c->chunk_elems = std::max<int64_t>(8, atoll(ce) / 8 * 8);  // tuning
     // default one-shot threshold: at N=2 one-shot moves the same NVLink bytes as two-shot
@@ -713,6 +735,7 @@ int gr_step(gr_ctx *c, int32_t *released, gr_cycle_info *info, uint32_t *global_
     p.group_bit_begin = c->d_gbb;
     p.group_bit_end = c->d_gbe;
     p.group_nchunks = c->d_gnch;
+    p.group_nsub = c->d_gnsub;
     p.group_elems = c->d_gel;
     p.big_groups = c->d_big;
     p.n_big = (int32_t)c->big_groups.size();
@@ -721,6 +744,7 @@ int gr_step(gr_ctx *c, int32_t *released, gr_cycle_info *info, uint32_t *global_
     p.out_released = c->d_rel_ring + (size_t)slot * c->G;
     p.out_cum = c->d_cum_ring + (size_t)slot * (c->G + 1);
     p.out_info = c->d_info_ring + slot;
+    p.out_subcum = c->d_subcum_ring + (size_t)slot * (c->G + 1);
     p.result = c->d_res;
     p.T = c->T;
     p.G = c->G;
@@ -765,6 +789,8 @@ int gr_step(gr_ctx *c, int32_t *released, gr_cycle_info *info, uint32_t *global_
         d.released = p.out_released;
         d.cum = p.out_cum;
         d.info = p.out_info;
+        d.subcum = p.out_subcum;
+        d.group_spc = c->d_gspc;
         d.dev_ptr = c->d_ptr;
         const int par = (int)(epoch & 1);
         d.nvls_uc = c->nvls.enabled ? reinterpret_cast<char *>(c->nvls.ucva) + (size_t)par * c->buf_parity_bytes : nullptr;
@@ -781,6 +807,7 @@ int gr_step(gr_ctx *c, int32_t *released, gr_cycle_info *info, uint32_t *global_
         d.abort_dev = c->d_counters + 2;
         d.err = c->d_err;
         d.trace = c->d_trace ? c->d_trace + (size_t)slot * c->trace_slot_u64 : nullptr;
+        d.trace_items = c->C * 4;  // u64 offset / 3 of the counters: counters start at 3*C*4
         d.chunk_begin = c->d_cbeg;
         d.chunk_end = c->d_cend;
         const int64_t es = c->buf_f16 ? 2 : 4;
@@ -803,6 +830,7 @@ int gr_step(gr_ctx *c, int32_t *released, gr_cycle_info *info, uint32_t *global_
         d.timeout_ns = (uint64_t)c->world.timeout_ms * 1000000ull;
         const bool local = c->N == 1;
         const int ctas = c->data_ctas[local ? gr::ALGO_LOCAL : gr::ALGO_TWOSHOT];
+        d.lc_sub = c->lc_sub;
         d.lag1 = c->lag1 > 0 ? c->lag1 : 2 * ctas;
         d.lag2 = c->lag2 > 0 ? c->lag2 : 4 * ctas;
         CK(c, cudaEventRecord(c->ev_bv, c->s_coord));
@@ -880,7 +908,8 @@ int gr_step(gr_ctx *c, int32_t *released, gr_cycle_info *info, uint32_t *global_
     const int complete = c->h_res->step_complete;
     const auto h_done = std::chrono::steady_clock::now();
     c->stats.host_step_us += std::chrono::duration<double, std::micro>(h_done - h_enter).count();
-    if (!c->trace_path.empty()) {
+    if (!c->trace_path.empty() && c->trace_written < c->trace_max) {
+        ++c->trace_written;
         auto ns = [](std::chrono::steady_clock::time_point t) {
             return (int64_t)std::chrono::duration_cast<std::chrono::nanoseconds>(t.time_since_epoch()).count();
         };
@@ -970,17 +999,35 @@ int gr_wait(gr_ctx *c) {
               << ",\"N\":" << c->N << ",\"k\":[" << tc.k_start << "," << tc.k_pop << "," << tc.k_and << ","
               << tc.k_end << "],\"h\":[" << tc.h_enter_ns << "," << tc.h_launched_ns << "," << tc.h_seen_ns
               << "," << tc.h_done_ns << "],\"n_released\":" << tc.n_released << ",\"algo\":" << tc.algo
-              << ",\"elems\":" << tc.elems << ",\"items\":[";
+              << ",\"elems\":" << tc.elems << ",\"nitems\":" << tc.nitems << ",\"items\":[";
             if (tc.nitems > 0) {
                 buf.resize((size_t)tc.nitems * 4);
                 CK(c, cudaMemcpy(buf.data(), c->d_trace + (size_t)tc.slot * c->trace_slot_u64,
                                  sizeof(uint64_t) * buf.size(), cudaMemcpyDeviceToHost));
+                bool first = true;
                 for (int i = 0; i < tc.nitems; ++i) {
-                    if (i) f << ",";
-                    f << "[" << buf[4 * i] << "," << buf[4 * i + 1] << "," << buf[4 * i + 2] << "," << buf[4 * i + 3] << "]";
+                    if (!buf[4 * i + 2]) continue;  // not executed on this rank
+                    if (!first) f << ",";
+                    first = false;
+                    f << "[" << i << "," << buf[4 * i] << "," << buf[4 * i + 1] << "," << buf[4 * i + 2] << ","
+                      << buf[4 * i + 3] << "]";
                 }
             }
-            f << "]}\n";
+            f << "]";
+            if (tc.nitems > 0 && c->N > 1) {  // xfer kernel per-CTA stall counters (clock64 cycles)
+                const int nct = c->data_ctas[gr::ALGO_TWOSHOT];
+                std::vector<uint64_t> pr((size_t)nct * 8);
+                CK(c, cudaMemcpy(pr.data(), c->d_trace + (size_t)tc.slot * c->trace_slot_u64 + (size_t)3 * c->C * 4,
+                                 sizeof(uint64_t) * pr.size(), cudaMemcpyDeviceToHost));
+                f << ",\"prof\":[";
+                for (int i = 0; i < nct; ++i) {
+                    if (i) f << ",";
+                    f << "[" << pr[8 * i] << "," << pr[8 * i + 1] << "," << pr[8 * i + 2] << "," << pr[8 * i + 3]
+                      << "," << pr[8 * i + 4] << "," << pr[8 * i + 5] << "]";
+                }
+                f << "]";
+            }
+            f << "}\n";
         }
         c->trace_cycles.clear();
     }

@@ -34,9 +34,22 @@ def main():
         print(f"  host us: pre-launch p50 {pct(hl,.5):.2f}  wait-for-handoff p50 {pct(hw,.5):.2f}  "
               f"post (data launch) p50 {pct(hd,.5):.2f}")
         for r in recs:
-            it = r["items"]
-            if not it:
+            raw = r["items"]
+            if not raw:
                 continue
+            # [item, grab, ready, done, cta|smid] (items never executed are omitted)
+            n = max(r.get("nitems", 0), max(x[0] for x in raw) + 1)
+            it = [[0, 0, 0, 0] for _ in range(n)]
+            for x in raw:
+                it[x[0]] = x[1:]
+            if r.get("prof"):
+                pf = [x for x in r["prof"] if x[0]]
+                if pf:
+                    tot = sum(x[0] for x in pf)
+                    ctot = sum(x[3] for x in pf) or 1
+                    print(f"    producer: ring-full stalls {100 * sum(x[1] for x in pf) / tot:.1f}%, "
+                          f"flag waits {100 * sum(x[2] for x in pf) / tot:.1f}% | consumers: starved (ring empty) "
+                          f"{100 * sum(x[4] for x in pf) / ctot:.1f}%, flag publish {100 * sum(x[5] for x in pf) / ctot:.1f}%")
             live = [x for x in it if x[0]]
             if not live:
                 continue
@@ -45,9 +58,8 @@ def main():
             ctas = len({x[3] & 0xffffffff for x in live})
             print(f"  cycle {r['cycle']} algo {r['algo']} elems {r['elems']} items {len(it)} ctas {ctas} "
                   f"span {(t1 - t0) / 1e3:.1f} us  (kernel-start -> first grab {(t0 - r['k'][3]) / 1e3:.1f} us after bv end)")
-            n = len(it)
-            nph = {1: 1, 2: 2, 3: 3}.get(r["algo"], 1)
-            per = n // nph
+            nph = {1: 1, 2: 2, 3: 3, 4: 3}.get(r["algo"], 1)
+            per = max(1, len(it) // nph)
             for ph in range(nph):
                 seg = [x for x in it[ph * per:(ph + 1) * per] if x[0] and x[2]]
                 if not seg:
