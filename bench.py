@@ -255,14 +255,16 @@ def main():
         torch.cuda.synchronize()
         st_timed = ctx.stats()
         clk.mark_timed_end()
+        ms_local = ev0.elapsed_time(ev1) / args.steps
         # the timed region is often far shorter than nvidia-smi's sampling period: keep the
-        # identical step running (untimed) for >= 1 s so the clock record covers this load
-        t_soak = time.perf_counter()
-        while time.perf_counter() - t_soak < 1.0:
+        # identical step running (untimed) for ~1 s so the clock record covers this load. The
+        # step count comes from the max-over-ranks time, so every rank runs the same number of
+        # collective steps.
+        n_soak = int(min(20000, max(1, 1000.0 / max(1e-3, max_over_ranks(ms_local)))))
+        for _ in range(n_soak):
             one_step()
         torch.cuda.synchronize()
     barrier()
-    ms_local = ev0.elapsed_time(ev1) / args.steps
     st = st_timed  # counters of exactly the K timed steps (the clock soak follows)
     ctx_nvls = "%s (%s)" % ctx.nvls() if N > 1 else None
     # the same steps with a host-blocking gr_wait (host latency exposed every step)

@@ -610,7 +610,8 @@ __global__ void __launch_bounds__(LC_THREADS, 3) local_kernel(DataParams p) {
 // whatever subset of CTAs is resident.
 // ---------------------------------------------------------------------------------------
 constexpr int XF_THREADS = 512;
-constexpr int XF_CONS = XF_THREADS - 32;
+constexpr int XF_CONS = XF_THREADS - 64;  // warp 0 producer, warp 1 publisher, warps 2.. consumers
+constexpr int XF_PUB = 8;                   // publication ring (chunk flags waiting for the fence)
 constexpr int XF_STAGES = 8;  // max ring depth (runtime depth: p.nstages)
 enum { K_PACK = 0, K_RED = 1, K_RS = 2, K_AG = 3, K_NRS = 5, K_STOP = 4 };
 
@@ -636,7 +637,6 @@ __device__ __forceinline__ void bulk_g2s(void *dst_smem, const void *src, uint32
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
                  ::"r"(smem_u32(dst_smem)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
 }
-__device__ __forceinline__ void consumer_sync() { asm volatile("bar.sync 1, %0;" ::"n"(XF_CONS) : "memory"); }
 
 // thread 0 of the producer: wait until *flag == epoch (or abort / timeout); false = abort
 __device__ __forceinline__ bool xf_wait_flag(const DataParams &p, const uint32_t *flag, int where) {
@@ -859,6 +859,8 @@ __global__ void __maxnreg__(96) xfer_kernel(DataParams p) {
     using B = Buf<BT>;
     extern __shared__ __align__(1024) char xsm[];
     __shared__ __align__(8) uint64_t full[XF_STAGES], empty[XF_STAGES];
+    __shared__ __align__(8) uint64_t pub_full[XF_PUB], pub_empty[XF_PUB];
+    __shared__ int pub_kind[XF_PUB], pub_chunk[XF_PUB];
     __shared__ XfMeta meta[XF_STAGES];
     __shared__ int s_cum[XF_RCACHE], s_cb[XF_RCACHE];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -868,6 +870,10 @@ __global__ void __maxnreg__(96) xfer_kernel(DataParams p) {
         for (int s = 0; s < XF_STAGES; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], XF_CONS / 32);
+        }
+        for (int s = 0; s < XF_PUB; ++s) {
+            mbar_init(&pub_full[s], XF_CONS / 32);
+            mbar_init(&pub_empty[s], 1);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -1058,12 +1064,51 @@ __global__ void __maxnreg__(96) xfer_kernel(DataParams p) {
                 pr[2] = (uint64_t)prof_flags;
             }
         }
+    } else if (warp == 1) {
+        // ---------------- publisher: takes finished chunks from the consumers (mbarrier ring,
+        // the consumers' stores are release-ordered before their arrive), makes them visible at
+        // system scope (fence.sc.sys waits for the stores) and pushes the chunk flags to the
+        // peers — the fence latency never stalls the consumer pipeline.
+        if (lane == 0) {
+            for (int ps = 0, ph = 0;; ) {
+                mbar_wait(&pub_full[ps], ph);
+                const int kind = pub_kind[ps], c = pub_chunk[ps];
+                if (kind == K_STOP) break;
+                fence_sys();
+                if (kind == K_RS || kind == K_NRS) {
+                    for (int q = 0; q < p.N; ++q)
+                        if (q != p.rank) st_relaxed_sys32(p.rs_flag[q] + c, p.epoch);
+                } else if (ALGO == ALGO_TWOSHOT || ALGO == ALGO_NVLS) {  // the owner (NVLS: possibly this rank)
+                    st_relaxed_sys32(p.pack_flag[c % p.N] + (size_t)c * p.N + p.rank, p.epoch);
+                } else {  // every rank, this one included: RED(c) must not overwrite g before PACK(c) read it
+                    for (int q = 0; q < p.N; ++q) st_relaxed_sys32(p.pack_flag[q] + (size_t)c * p.N + p.rank, p.epoch);
+                }
+                mbar_arrive(&pub_empty[ps]);
+                if (++ps == XF_PUB) { ps = 0; ph ^= 1; }
+            }
+        }
     } else {
-        const int ct = tid - 32;  // consumer thread index
+        const int ct = tid - 64;  // consumer thread index
         int stage = 0;
         uint32_t ph = 0;
+        int ps = 0;
+        uint32_t pph = 1;  // publication slots start free
         long long prof_full = 0, prof_flag = 0;
         const long long prof_t0 = clock64();
+        // hand a finished chunk (or the stop message) to the publisher
+        auto publish = [&](int kind, int c) {
+            const long long t0 = clock64();
+            if (lane == 0) mbar_wait(&pub_empty[ps], pph);
+            __syncwarp();
+            if (ct == 0) {
+                pub_kind[ps] = kind;
+                pub_chunk[ps] = c;
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&pub_full[ps]);  // release: this warp's stores, ct 0's meta
+            if (++ps == XF_PUB) { ps = 0; pph ^= 1; }
+            prof_flag += clock64() - t0;
+        };
         for (;;) {
             {
                 const long long t0 = clock64();
@@ -1084,22 +1129,7 @@ __global__ void __maxnreg__(96) xfer_kernel(DataParams p) {
             // the stage is free once every consumer warp has read it
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[stage]);
-            if (last && (kind == K_PACK || kind == K_RS || kind == K_NRS)) {  // chunk done: publish its flag
-                const long long t0 = clock64();
-                consumer_sync();
-                if (ct == 0) {
-                    fence_sys();
-                    if (kind == K_RS || kind == K_NRS) {
-                        for (int q = 0; q < p.N; ++q)
-                            if (q != p.rank) st_relaxed_sys32(p.rs_flag[q] + c, p.epoch);
-                    } else if (ALGO == ALGO_TWOSHOT || ALGO == ALGO_NVLS) {  // the owner (NVLS: possibly this rank)
-                        st_relaxed_sys32(p.pack_flag[c % p.N] + (size_t)c * p.N + p.rank, p.epoch);
-                    } else {  // every rank, this one included: RED(c) must not overwrite g before PACK(c) read it
-                        for (int q = 0; q < p.N; ++q) st_relaxed_sys32(p.pack_flag[q] + (size_t)c * p.N + p.rank, p.epoch);
-                    }
-                }
-                prof_flag += clock64() - t0;
-            }
+            if (last && (kind == K_PACK || kind == K_RS || kind == K_NRS)) publish(kind, c);
             if (p.trace && last && ct == 0) {
                 uint32_t smid;
                 asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
@@ -1108,6 +1138,7 @@ __global__ void __maxnreg__(96) xfer_kernel(DataParams p) {
             }
             if (++stage == nst) { stage = 0; ph ^= 1; }
         }
+        publish(K_STOP, 0);
         if (p.trace && ct == 0) {
             uint64_t *pr = p.trace + (size_t)3 * p.trace_items + (size_t)blockIdx.x * 8;
             pr[3] = (uint64_t)(clock64() - prof_t0);
