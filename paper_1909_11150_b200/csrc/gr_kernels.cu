@@ -76,14 +76,17 @@ constexpr int BV_BATCH = GR_BV_BATCH;
 
 // Shared memory: sL[W] local bitvector, sA[W] intersection, sR[W] released-tensor bits of
 // this step, sC[Gw] complete-group bits (Gw = ceil(G/32)).
-__global__ void __launch_bounds__(BV_THREADS, 4) bitvector_kernel(BvParams p) {
+// Two instantiations: 256 threads (small bitvectors; 56 registers, co-resident with a running
+// reduction) and 1024 threads (W > 64 words, i.e. more than ~2000 tensors).
+template <int NT>
+__global__ void __launch_bounds__(NT, 1024 / NT) bitvector_kernel(BvParams p) {
     extern __shared__ uint32_t smem[];
     const int W = p.W, G = p.G, Gw = (p.G + 31) / 32;
     uint32_t *sL = smem, *sA = smem + W, *sR = smem + 2 * W, *sC = smem + 3 * W;
     __shared__ int s_timeout;
-    __shared__ int s_scan[BV_THREADS / 32][3];
+    __shared__ int s_scan[NT / 32][3];
     __shared__ unsigned long long s_elems;
-    __shared__ int s_all[BV_THREADS / 32];
+    __shared__ int s_all[NT / 32];
     __shared__ int s_tot[3];
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
@@ -130,23 +133,33 @@ __global__ void __launch_bounds__(BV_THREADS, 4) bitvector_kernel(BvParams p) {
     // LL words (tag|word) read straight from the peers' slots over NVLink, all loads issued
     // before any is consumed; a stale tag (peer not yet in this cycle) is re-polled. ----
     const uint64_t deadline = globaltimer() + p.timeout_ns;
-    for (int w = tid; w < W; w += blockDim.x) {
-        uint64_t raw[GR_MAX_RANKS];
+    constexpr int AB = NT >= 1024 ? 1 : 2;  // words per thread with all their peer loads in flight together
+    for (int w0 = tid; w0 < W; w0 += blockDim.x * AB) {
+        uint64_t raw[AB][GR_MAX_RANKS];
 #pragma unroll
-        for (int r = 0; r < GR_MAX_RANKS; ++r)
-            raw[r] = (r < p.N && r != p.rank) ? ld_relaxed_sys64(p.slot[r] + (size_t)p.parity * W + w) : 0ull;
-        uint32_t a = sL[w];
+        for (int k = 0; k < AB; ++k) {
+            const int w = w0 + k * blockDim.x;
 #pragma unroll
-        for (int r = 0; r < GR_MAX_RANKS; ++r) {
-            if (r >= p.N || r == p.rank) continue;
-            uint64_t x = raw[r];
-            while ((uint32_t)(x >> 32) != p.tag) {
-                if (globaltimer() > deadline) { s_timeout = 1; break; }
-                x = ld_relaxed_sys64(p.slot[r] + (size_t)p.parity * W + w);
-            }
-            a &= (uint32_t)x;
+            for (int r = 0; r < GR_MAX_RANKS; ++r)
+                raw[k][r] = (w < W && r < p.N && r != p.rank) ? ld_relaxed_sys64(p.slot[r] + (size_t)p.parity * W + w) : 0ull;
         }
-        sA[w] = a;
+#pragma unroll
+        for (int k = 0; k < AB; ++k) {
+            const int w = w0 + k * blockDim.x;
+            if (w >= W) break;
+            uint32_t a = sL[w];
+#pragma unroll
+            for (int r = 0; r < GR_MAX_RANKS; ++r) {
+                if (r >= p.N || r == p.rank) continue;
+                uint64_t x = raw[k][r];
+                while ((uint32_t)(x >> 32) != p.tag) {
+                    if (globaltimer() > deadline) { s_timeout = 1; break; }
+                    x = ld_relaxed_sys64(p.slot[r] + (size_t)p.parity * W + w);
+                }
+                a &= (uint32_t)x;
+            }
+            sA[w] = a;
+        }
     }
     __syncthreads();
     const uint64_t t_anded = globaltimer();
@@ -295,10 +308,12 @@ int launch_bitvector(const BvParams &p, void *stream) {
     const size_t smem = sizeof(uint32_t) * (3 * (size_t)p.W + ((size_t)p.G + 31) / 32);
     static bool attr_set = false;
     if (!attr_set) {
-        cudaFuncSetAttribute(bitvector_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+        cudaFuncSetAttribute(bitvector_kernel<BV_THREADS>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+        cudaFuncSetAttribute(bitvector_kernel<1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
         attr_set = true;
     }
-    bitvector_kernel<<<1, BV_THREADS, smem, (cudaStream_t)stream>>>(p);
+    if (p.W > GR_BV_INLINE_WORDS) bitvector_kernel<1024><<<1, 1024, smem, (cudaStream_t)stream>>>(p);
+    else bitvector_kernel<BV_THREADS><<<1, BV_THREADS, smem, (cudaStream_t)stream>>>(p);
     return (int)cudaGetLastError();
 }
 

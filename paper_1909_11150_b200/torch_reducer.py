@@ -1,0 +1,92 @@
+"""PyTorch integration: the paper's gradient path inside a real
+autograd backward pass.
+
+`GroupedGradReducer` registers a post-accumulate-grad hook on every parameter; the hook marks
+the gradient ready with `gr_mark_ready_async` on the stream autograd is using, so the ready
+flag is written by the GPU right after the gradient exists ("pending requests").
+`synchronize()` then runs coordination cycles ("tics") until every group has been
+released — complete groups are reduced while the GPU is still running the rest of the backward
+pass — and makes the current stream wait for the reduced gradients (no host block).
+
+Argument marshalling only: all arithmetic runs in libgr.so. Groups default to the paper's
+usage — a few contiguous groups of roughly equal bytes in reverse registration order (the
+order backward produces gradients; SPEC.md:296 default), or explicit per-parameter group ids
+("explicit assignment of collective operations into groups").
+"""
+from __future__ import annotations
+
+import time
+
+import torch
+
+from .binding import GR_F16, Context, make_allgather
+
+
+def contiguous_groups(numels, n_groups: int):
+    """Group ids for tensors listed in registration order: G contiguous runs of about equal
+    element count over the REVERSE order (the order backward produces gradients), numbered in
+    that production order (group 0 is ready first)."""
+    T = len(numels)
+    n_groups = max(1, min(n_groups, T))
+    total = float(sum(numels))
+    gid = [0] * T
+    acc = 0.0
+    g = 0
+    for i, t in enumerate(reversed(range(T))):
+        gid[t] = g
+        acc += numels[t]
+        remaining_tensors = T - i - 1
+        if acc >= (g + 1) * total / n_groups and g < n_groups - 1 and remaining_tensors >= n_groups - 1 - g:
+            g += 1
+    # make ids dense (a group may have ended up empty on tiny tables)
+    remap = {v: k for k, v in enumerate(sorted(set(gid)))}
+    return [remap[v] for v in gid]
+
+
+class GroupedGradReducer:
+    def __init__(self, params, *, rank: int, world_size: int, device: int, groups=None, n_groups: int = 4,
+                 buffer_dtype: int = GR_F16, pg=None, timeout_ms: int = 0, comm_ctas: int = 0):
+        self.params = [p for p in params if p.requires_grad]
+        numels = [p.numel() for p in self.params]
+        self.group_of = list(groups) if groups is not None else contiguous_groups(numels, n_groups)
+        grad_f16 = [p.dtype == torch.float16 for p in self.params]
+        if any(p.dtype not in (torch.float32, torch.float16) for p in self.params):
+            raise TypeError("GroupedGradReducer supports fp32 and fp16 parameters")
+        self.world_size = world_size
+        self._ag = make_allgather(pg, device) if world_size > 1 else None
+        self.ctx = Context(rank=rank, world_size=world_size, device=device, numel=numels, group_of=self.group_of,
+                           grad_f16=grad_f16, buffer_dtype=buffer_dtype,
+                           compute_stream=torch.cuda.current_stream(device).cuda_stream, timeout_ms=timeout_ms,
+                           comm_ctas=comm_ctas, allgather=self._ag)
+        self.cycles_last_step = 0
+        self._hooks = [p.register_post_accumulate_grad_hook(self._make_hook(t)) for t, p in enumerate(self.params)]
+
+    def _make_hook(self, t: int):
+        def hook(p):
+            # stream-ordered readiness: the flag is written after the accumulation kernel
+            self.ctx.gr_mark_ready_async(t, p.grad.data_ptr(), torch.cuda.current_stream(p.device).cuda_stream)
+        return hook
+
+    def synchronize(self, cycle_us: float = 0.0, max_cycles: int = 1_000_000):
+        """Run coordination cycles until the step's gradients are all released, then order the
+        current stream after their reduction. Returns the number of cycles."""
+        n = 0
+        nxt = time.perf_counter()
+        while n < max_cycles:
+            _rel, complete, _bits, _info = self.ctx.gr_step()
+            n += 1
+            if complete:
+                break
+            if cycle_us > 0:
+                nxt += cycle_us * 1e-6
+                while time.perf_counter() < nxt:
+                    pass
+        self.ctx.gr_wait_async()
+        self.cycles_last_step = n
+        return n
+
+    def close(self):
+        for h in self._hooks:
+            h.remove()
+        self._hooks = []
+        self.ctx.gr_finalize()

@@ -266,3 +266,39 @@ def test_multi_gpu_grad_stats(n):
     if gpu_count() < n:
         pytest.skip(f"needs {n} GPUs")
     assert _torchrun(n, "--suite", "stats", "--seeds", "0:3") == 0
+
+
+def test_autograd_reducer_n1(gpu):
+    """NEXT-3 at N=1: hooks mark the gradients during backward; after synchronize() each
+    gradient equals fl32(fl16(plain-backward gradient)) bit for bit (reading R7-R9 at N=1)."""
+    import torch
+    from harness.fcdensenet import batch, make_model
+    from paper_1909_11150_b200.torch_reducer import GroupedGradReducer
+    torch.backends.cudnn.deterministic = True  # the reference backward must reproduce the gradients
+    torch.backends.cudnn.benchmark = False
+    model, ref = make_model(3, gpu), make_model(3, gpu)
+    red = GroupedGradReducer(model.parameters(), rank=0, world_size=1, device=0, n_groups=3)
+    for step in range(3):
+        x, y = batch(step, 0, gpu)
+        model.zero_grad(set_to_none=False)
+        ref.load_state_dict(model.state_dict())
+        ref.zero_grad(set_to_none=False)
+        torch.nn.functional.mse_loss(model(x), y).backward()
+        red.synchronize()
+        torch.nn.functional.mse_loss(ref(x), y).backward()
+        torch.cuda.synchronize()
+        for a, b in zip(model.parameters(), ref.parameters()):
+            assert torch.equal(a.grad, b.grad.half().float())
+        with torch.no_grad():
+            for p in model.parameters():
+                p -= 0.05 * p.grad
+    red.close()
+
+
+@pytest.mark.parametrize("n", [2, 4, 8])
+def test_multi_gpu_autograd_reducer(n):
+    """NEXT-3 at N ranks: backward hooks + cycles on a small FC-DenseNet; reduced gradients vs
+    the fp64 average of the plain-backward gradients, replicas identical through SGD steps."""
+    if gpu_count() < n:
+        pytest.skip(f"needs {n} GPUs")
+    assert _torchrun(n, "--suite", "autograd", "--seeds", "0:1", "--buffers", "f16") == 0

@@ -48,3 +48,24 @@ def test_values_numpy_torch_identical():
     # sampled indices equal the dense fill
     idx = np.array([0, 5, 69999, 123])
     assert np.array_equal(values_np(5, 2, 1, idx, float(s[1])), values_np(5, 2, 1, np.arange(70000), float(s[1]))[idx])
+
+
+def test_contiguous_groups():
+    from paper_1909_11150_b200.torch_reducer import contiguous_groups
+    rng = np.random.default_rng(0)
+    for _ in range(200):
+        T = int(rng.integers(1, 40))
+        G = int(rng.integers(1, 10))
+        numel = rng.integers(1, 1000, size=T).tolist()
+        g = contiguous_groups(numel, G)
+        assert sorted(set(g)) == list(range(max(g) + 1)) and max(g) < min(G, T)
+        rev = list(reversed(g))  # production (reverse) order: non-decreasing group ids
+        assert rev == sorted(rev)
+
+
+def test_tiny_fcdensenet_cpu():
+    import torch
+    from harness.fcdensenet import batch, make_model
+    m = make_model(0, "cpu")
+    x, y = batch(0, 0, "cpu")
+    assert m(x).shape == y.shape

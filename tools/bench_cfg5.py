@@ -76,7 +76,12 @@ def main():
                              one_shot_max_bytes=osm, timeout_ms=30000, allgather=ag)
             batch = ctx.prepare_batch([0], [g.data_ptr()])
 
-            def ours():
+            def ours():  # stream-ordered wait: the production contract (host never blocks on the data)
+                ctx.gr_mark_ready_prepared(batch)
+                ctx.gr_step()
+                ctx.gr_wait_async()
+
+            def ours_blocking():
                 ctx.gr_mark_ready_prepared(batch)
                 ctx.gr_step()
                 ctx.gr_wait()
@@ -84,6 +89,8 @@ def main():
             ms = timed(ours, iters)
             res[f"{name}_us"] = ms * 1e3
             res[f"{name}_busbw"] = S * 2 * (N - 1) / N / (ms * 1e-3) / 1e9
+            if name == "default":
+                res["default_blocking_us"] = timed(ours_blocking, iters) * 1e3
             ctx.gr_finalize()
         x = torch.zeros(n, dtype=torch.float16 if pb == 2 else torch.float32, device=dev)
         ms = timed(lambda: dist.all_reduce(x, op=dist.ReduceOp.AVG), iters)
@@ -94,7 +101,8 @@ def main():
             print(json.dumps({k: (round(v, 3) if isinstance(v, float) else v) for k, v in res.items()}), flush=True)
     if rank == 0:
         print(json.dumps({"cfg5_summary": True, "N": N, "buffer": a.buffer,
-                          "what": "ours = mark+gr_step+fused pack/reduce/unpack+gr_wait on one fp32 tensor; "
+                          "what": "ours = mark+gr_step+fused pack/reduce/unpack+gr_wait_async on one fp32 tensor "
+                                  "(default_blocking_us: with the host-blocking gr_wait); "
                                   "nccl = all_reduce(AVG) on a same-size buffer-dtype tensor (reduce only)"}))
     dist.destroy_process_group()
 
