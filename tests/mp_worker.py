@@ -55,7 +55,10 @@ def autograd_suite(rank, N, local, dev):
             dist.all_gather(g_all, mine)  # gloo process group: CPU tensors
             stack = torch.stack(g_all)
             want = stack.mean(0)
-            tol = 2.0 ** -10 * N * float(stack.abs().max()) + 1e-30
+            # north-star fp16 bound plus the fp16 subnormal quantum: real gradients of this toy
+            # model reach |g| ~ 1e-6, where RN to fp16 has absolute error up to 2^-25 per rounding
+            # (input + output rounding -> 2^-24); R11
+            tol = 2.0 ** -10 * N * float(stack.abs().max()) + 2.0 ** -24
             err = float((p_ours.grad.double().cpu() - want).abs().max())
             if err > tol:
                 ok = False

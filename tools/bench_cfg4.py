@@ -8,7 +8,9 @@ rotation reaches it), T/16 marks per cycle. The last rank is a straggler that en
 gr_step delta us late every cycle. Reported per T: host latency of gr_step (p50/p99; for
 the straggler this is last arrival -> its result), the bitvector kernel's own span
 (%globaltimer), and the same-box baselines: NCCL all_reduce(MIN) on u8[T] ready flags
-(NCCL has no bitwise AND) and gloo all_reduce(BAND) on u32[W] (the paper's MPI_BAND).
+(NCCL has no bitwise AND), gloo all_reduce(BAND) on u32[W] (the paper's MPI_BAND), and the
+paper's original master-worker coordination (harness/master_worker.py: Gatherv of serialized
+requests to rank 0, intersect, Bcast of ordered responses; gloo on the host CPU).
 """
 import argparse
 import json
@@ -37,6 +39,7 @@ def main():
     import torch.distributed as dist
 
     import paper_1909_11150_b200 as gr
+    from harness.master_worker import MasterWorker
     from workloads import cfg4_case
 
     rank = int(os.environ["RANK"])
@@ -118,10 +121,29 @@ def main():
             t0 = time.perf_counter()
             dist.all_reduce(words, op=dist.ReduceOp.BAND, group=gloo)
             gl.append((time.perf_counter() - t0) * 1e6)
+        # the paper's original strategy (NEXT-4): master-worker gather -> intersect -> broadcast
+        # of serialized requests/responses over gloo, same schedule, every cycle timed
+        mw = MasterWorker(rank, N, case.group_of, pg=gloo)
+        ml, mcyc = [], 0
+        dist.barrier(group=gloo)
+        while mcyc < min(a.cycles, 600):
+            c = 0
+            while True:
+                t0 = time.perf_counter()
+                _ids, complete = mw.cycle(order.get(c, []))
+                ml.append((time.perf_counter() - t0) * 1e6)
+                c += 1
+                mcyc += 1
+                if complete:
+                    break
+        mw_p50 = torch.tensor([pct(ml, 0.5)], dtype=torch.float64)
+        dist.all_reduce(mw_p50, op=dist.ReduceOp.MAX, group=gloo)
         if rank == 0:
             print(json.dumps({"T": T, "N": N, "baseline": True,
                               "nccl_min_u8_us_p50": round(pct(nl[50:], 0.5), 2),
-                              "gloo_band_u32_us_p50": round(pct(gl[50:], 0.5), 2)}), flush=True)
+                              "gloo_band_u32_us_p50": round(pct(gl[50:], 0.5), 2),
+                              "master_worker_us_p50": round(float(mw_p50), 2),
+                              "master_worker_cycles": len(ml)}), flush=True)
         T *= 4
     dist.destroy_process_group()
 

@@ -24,6 +24,7 @@ def main():
     ap.add_argument("--min-kib", type=int, default=1)
     ap.add_argument("--max-mib", type=int, default=1024)
     ap.add_argument("--iters", type=int, default=20)
+    ap.add_argument("--quick", action="store_true", help="library default only, no NCCL (tuning sweeps)")
     a = ap.parse_args()
 
     import torch
@@ -70,7 +71,8 @@ def main():
         iters = a.iters if S <= (64 << 20) else max(5, a.iters // 4)
         g = torch.randn(n, device=dev)
         res = {"bytes": S, "elems": n}
-        for name, osm in (("default", -1), ("oneshot", 1 << 62), ("twoshot", 0)):
+        variants = (("default", -1),) if a.quick else (("default", -1), ("oneshot", 1 << 62), ("twoshot", 0))
+        for name, osm in variants:
             ctx = gr.Context(rank=rank, world_size=N, device=local, numel=[n], group_of=[0],
                              buffer_dtype=gr.GR_F16 if pb == 2 else gr.GR_F32, compute_stream=comp.cuda_stream,
                              one_shot_max_bytes=osm, timeout_ms=30000, allgather=ag)
@@ -89,13 +91,14 @@ def main():
             ms = timed(ours, iters)
             res[f"{name}_us"] = ms * 1e3
             res[f"{name}_busbw"] = S * 2 * (N - 1) / N / (ms * 1e-3) / 1e9
-            if name == "default":
+            if name == "default" and not a.quick:
                 res["default_blocking_us"] = timed(ours_blocking, iters) * 1e3
             ctx.gr_finalize()
-        x = torch.zeros(n, dtype=torch.float16 if pb == 2 else torch.float32, device=dev)
-        ms = timed(lambda: dist.all_reduce(x, op=dist.ReduceOp.AVG), iters)
-        res["nccl_us"] = ms * 1e3
-        res["nccl_busbw"] = S * 2 * (N - 1) / N / (ms * 1e-3) / 1e9
+        if not a.quick:
+            x = torch.zeros(n, dtype=torch.float16 if pb == 2 else torch.float32, device=dev)
+            ms = timed(lambda: dist.all_reduce(x, op=dist.ReduceOp.AVG), iters)
+            res["nccl_us"] = ms * 1e3
+            res["nccl_busbw"] = S * 2 * (N - 1) / N / (ms * 1e-3) / 1e9
         rows.append(res)
         if rank == 0:
             print(json.dumps({k: (round(v, 3) if isinstance(v, float) else v) for k, v in res.items()}), flush=True)
