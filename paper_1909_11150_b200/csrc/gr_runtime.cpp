@@ -34,7 +34,6 @@ namespace {
 
 thread_local std::string g_init_error = "no error";
 
-constexpr int64_t kMaxChunkElems = 131072;  // largest adaptive chunk (elements)
 constexpr int32_t kDefaultTimeoutMs = 20000;
 constexpr size_t kAlign = 256;
 
@@ -59,6 +58,7 @@ struct gr_ctx {
     bool dry = false;
     int buf_f16 = 1;
     int64_t chunk_elems = 0;  // 0 = adaptive per group
+    int64_t chunk_target_div = 296, chunk_max = 131072;  // adaptive rule (GR_CHUNK_DIV / GR_CHUNK_MAX)
     int64_t one_shot_max_bytes = 0;
     uint64_t hash = 0;
 
@@ -267,9 +267,9 @@ int build_layouts(gr_ctx *c, const gr_tensor *table, const int32_t *group_of) {
         // large items (fewer flags, longer TMA streams), small ones keep every SM busy
         int64_t cg = c->chunk_elems;
         if (cg == 0) {
-            const int64_t target = std::max<int64_t>(1, (gend[g] - gbeg[g]) / 296);
+            const int64_t target = std::max<int64_t>(1, (gend[g] - gbeg[g]) / c->chunk_target_div);
             cg = 8192;
-            while (cg * 2 <= target && cg < 131072) cg *= 2;
+            while (cg * 2 <= target && cg < c->chunk_max) cg *= 2;
         }
         for (int64_t cb = gbeg[g]; cb < gend[g]; cb += cg) {
             const int64_t ce = std::min(gend[g], cb + cg);
@@ -568,6 +568,8 @@ int gr_init(gr_ctx **out, const gr_world *world, const gr_tensor *table, int32_t
     c->buf_f16 = world->buffer_dtype == GR_F16;
     c->chunk_elems = world->chunk_elems;  // 0: adaptive per group (build_layouts)
     if (const char *ls = getenv("GR_LC_SUB")) c->lc_sub = std::max<int64_t>(256, atoll(ls) / 8 * 8);  // tuning
+    if (const char *cd = getenv("GR_CHUNK_DIV")) c->chunk_target_div = std::max<int64_t>(1, atoll(cd));  // tuning
+    if (const char *cm = getenv("GR_CHUNK_MAX")) c->chunk_max = std::max<int64_t>(8192, atoll(cm));      // tuning
     if (world->chunk_elems == 0)
         if (const char *ce = getenv("GR_CHUNK_ELEMS")) c->chunk_elems = std::max<int64_t>(8, atoll(ce) / 8 * 8);  // tuning
     // default one-shot threshold: at N=2 one-shot moves the same NVLink bytes as two-shot
@@ -816,7 +818,7 @@ int gr_step(gr_ctx *c, int32_t *released, gr_cycle_info *info, uint32_t *global_
         d.nstages = c->nstages;
         // RED/RS stage: N-1 peer slots (buffer precision) + one fp32-spaced gradient slot
         int64_t sr = c->N > 1 ? stage / ((c->N - 1) * es + 4) / 256 * 256 : 256;
-        const int64_t cmax = c->chunk_elems > 0 ? c->chunk_elems : kMaxChunkElems;
+        const int64_t cmax = c->chunk_elems > 0 ? c->chunk_elems : c->chunk_max;
         sr = std::max<int64_t>(256, std::min<int64_t>(sr, cmax));
         d.sub_red = sr;
         d.slot_bytes_red = sr * es;
