@@ -165,6 +165,15 @@ int gr_wait(gr_ctx *ctx);
  * at the next gr_step / gr_wait. With GR_TRACE set it behaves like gr_wait. */
 int gr_wait_async(gr_ctx *ctx);
 
+/* gr_released_wait_async — LOCAL. Makes `stream` (a cudaStream_t; NULL = world.compute_stream)
+ * wait for the reduction of every group released so far in this step, without ending the step
+ * or blocking the host: work enqueued on `stream` afterwards sees those groups' reduced
+ * gradients (e.g. a device->host copy or an optimizer update of the layers whose gradients are
+ * final while later groups are still pending). PAPER.md:110: the operations released at a tic
+ * are executed at that tic; this exposes their completion per cycle. GR_ESTATE on a dry
+ * context or in a sticky error state. */
+int gr_released_wait_async(gr_ctx *ctx, void *stream);
+
 /* gr_set_status — LOCAL. Raise (1) or clear (0) this rank's ABORT / SHUTDOWN
  * status bit for the following cycles (PAPER.md:130 reserved status bits). */
 int gr_set_status(gr_ctx *ctx, int32_t abort_flag, int32_t shutdown_flag);

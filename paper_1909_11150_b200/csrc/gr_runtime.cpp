@@ -78,7 +78,7 @@ struct gr_ctx {
     // device state
     int dev = -1;
     cudaStream_t s_coord = nullptr, s_data = nullptr, s_compute = nullptr;
-    cudaEvent_t ev_compute = nullptr, ev_data_done = nullptr, ev_bv = nullptr;
+    cudaEvent_t ev_compute = nullptr, ev_data_done = nullptr, ev_bv = nullptr, ev_released = nullptr;
     cudaEvent_t ring_ev[GR_SLOT_RING] = {};
     bool ring_pending[GR_SLOT_RING] = {};
     char *symm = nullptr;
@@ -354,6 +354,7 @@ int setup_device(gr_ctx *c) {
     c->s_compute = (cudaStream_t)c->world.compute_stream;
     CK(c, cudaEventCreateWithFlags(&c->ev_compute, cudaEventDisableTiming));
     CK(c, cudaEventCreateWithFlags(&c->ev_data_done, cudaEventDisableTiming));
+    CK(c, cudaEventCreateWithFlags(&c->ev_released, cudaEventDisableTiming));
     CK(c, cudaEventCreateWithFlags(&c->ev_bv, cudaEventDisableTiming));
     for (int i = 0; i < GR_SLOT_RING; ++i) CK(c, cudaEventCreateWithFlags(&c->ring_ev[i], cudaEventDisableTiming));
 
@@ -505,6 +506,7 @@ void free_all(gr_ctx *c) {
         if (c->ring_ev[i]) cudaEventDestroy(c->ring_ev[i]);
     if (c->ev_compute) cudaEventDestroy(c->ev_compute);
     if (c->ev_data_done) cudaEventDestroy(c->ev_data_done);
+    if (c->ev_released) cudaEventDestroy(c->ev_released);
     if (c->ev_bv) cudaEventDestroy(c->ev_bv);
     for (auto &v : {c->pending_data_ev, c->pending_bv_ev, c->free_ev})
         for (auto &pr : v) {
@@ -973,6 +975,17 @@ int gr_wait_async(gr_ctx *c) {
     CK(c, cudaEventRecord(c->ev_data_done, c->s_data));
     CK(c, cudaStreamWaitEvent(c->s_compute, c->ev_data_done, 0));
     return start_next_step(c);
+}
+
+int gr_released_wait_async(gr_ctx *c, void *stream) {
+    if (!c) return GR_EINVAL;
+    if (c->dry) return fail(c, GR_ESTATE, "dry context (device < 0) cannot wait");
+    if (c->sticky == GR_ECUDA) return fail(c, GR_ESTATE, "context is in a sticky error state: %s", c->err.c_str());
+    CK(c, cudaSetDevice(c->dev));
+    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : c->s_compute;
+    CK(c, cudaEventRecord(c->ev_released, c->s_data));  // data kernels are serialized on s_data
+    CK(c, cudaStreamWaitEvent(s, c->ev_released, 0));
+    return GR_OK;
 }
 
 int gr_wait(gr_ctx *c) {

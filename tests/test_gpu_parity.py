@@ -204,6 +204,31 @@ def test_async_marks_follow_stream(gpu):
     ctx.gr_finalize()
 
 
+def test_released_wait_async_orders_copy_out(gpu):
+    """gr_released_wait_async: a side stream that waits on it sees each released group's
+    reduced values while later groups are still pending (fp16 buffer at N=1: fl32(fl16(g)))."""
+    import torch
+    from paper_1909_11150_b200 import GR_F16, Context
+    n = 1 << 22
+    xs = [torch.randn(n, device=gpu) * (i + 1) for i in range(3)]
+    want = [x.half().float() for x in xs]
+    ctx = Context(rank=0, world_size=1, device=0, numel=[n] * 3, group_of=[0, 1, 2], buffer_dtype=GR_F16)
+    side = torch.cuda.Stream(device=gpu)
+    outs = [torch.empty_like(x) for x in xs]
+    for g in range(3):
+        ctx.gr_mark_ready(g, xs[g].data_ptr())
+        rel, complete, _, _ = ctx.gr_step()
+        assert rel == [g] and complete == (g == 2)
+        ctx.gr_released_wait_async(side.cuda_stream)
+        with torch.cuda.stream(side):
+            outs[g].copy_(xs[g])
+    side.synchronize()
+    for g in range(3):
+        assert torch.equal(outs[g], want[g]), g
+    ctx.gr_wait()
+    ctx.gr_finalize()
+
+
 def test_fcn220m_n1_full_size(gpu):
     """The bench workload at full size (225,115,137 elements, 68 tensors,
     10 groups), reverse-layer schedule; values checked on sampled elements."""
