@@ -1,3 +1,3 @@
-timeout 600 python -m pytest tests/test_gpu_parity.py -q -x -k "released or async or autograd_reducer_n1" > gpurun_out/pt_rel.log 2>&1
-timeout 600 python bench.py > gpurun_out/bench_n1.json 2> gpurun_out/bench_n1.err
-timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29666 bench.py --gpus 2 > gpurun_out/bench_n2.json 2> gpurun_out/bench_n2.err
+timeout 300 python bench.py --steps 3 --warmup 3 --no-extras > gpurun_out/plain.json 2>&1 && \
+timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none -c 1500 --csv --log-file gpurun_out/r01b_n1_launches.csv python bench.py --steps 3 --warmup 3 --no-extras > gpurun_out/ncu_l.log 2>&1
+echo rc=$?
