@@ -574,13 +574,14 @@ int gr_init(gr_ctx **out, const gr_world *world, const gr_tensor *table, int32_t
     if (const char *cm = getenv("GR_CHUNK_MAX")) c->chunk_max = std::max<int64_t>(8192, atoll(cm));      // tuning
     if (world->chunk_elems == 0)
         if (const char *ce = getenv("GR_CHUNK_ELEMS")) c->chunk_elems = std::max<int64_t>(8, atoll(ce) / 8 * 8);  // tuning
-    // default one-shot threshold: at N=2 one-shot moves the same NVLink bytes as two-shot
-    // with one fewer synchronisation, so it is used at every size; above N=2 it is kept for
-    // latency-bound messages.
     // default one-shot threshold: one-shot (every rank reads all N-1 peer copies) has the
     // fewest synchronisations; two-shot moves 2(N-1)/N of the message per direction and less
-    // local HBM traffic, and wins for large messages at every N (measured).
-    c->one_shot_max_bytes = world->one_shot_max_bytes >= 0 ? world->one_shot_max_bytes : (int64_t)1 << 20;
+    // local HBM traffic. Crossover measured with tools/bench_cfg5.py (profiles/r01_cfg):
+    // N=2 between 128 and 256 MiB, N=4 at ~8 MiB; N>=8 reads 7 peer copies, kept at 1 MiB.
+    {
+        const int64_t thr = c->N <= 2 ? (128ll << 20) : c->N == 3 ? (32ll << 20) : c->N == 4 ? (8ll << 20) : (1ll << 20);
+        c->one_shot_max_bytes = world->one_shot_max_bytes >= 0 ? world->one_shot_max_bytes : thr;
+    }
     c->dry = world->device < 0;
     if (c->world.timeout_ms <= 0) c->world.timeout_ms = kDefaultTimeoutMs;
     int rc = build_layouts(c, table, group_of);

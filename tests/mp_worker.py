@@ -185,7 +185,9 @@ def main():
                 mark = reverse_layer_schedule(len(f.layers), N, f.release_order, layers_per_cycle=1,
                                               jitter_seed=s0, max_shift=2)
                 case = Case(N, f.numel, f.group_of, mark, s0)
-                run(case, s0, buf)
+                run(case, s0, buf)              # library default (one-shot below the crossover)
+                if buf == "f16" and os.environ.get("GR_NVLS") != "1":
+                    run(case, s0, buf, osm=0)   # every group through the two-shot path
             else:
                 raise SystemExit(f"unknown suite {args.suite}")
     except Exception:

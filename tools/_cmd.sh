@@ -1,3 +1,3 @@
-timeout 300 python bench.py --steps 3 --warmup 3 --no-extras > gpurun_out/plain.json 2>&1 && \
-timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none -c 1500 --csv --log-file gpurun_out/r01b_n1_launches.csv python bench.py --steps 3 --warmup 3 --no-extras > gpurun_out/ncu_l.log 2>&1
-echo rc=$?
+timeout 1300 python -m pytest tests -m gpu -q -x > gpurun_out/pt4.log 2>&1; tail -3 gpurun_out/pt4.log
+timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 --master-port 29667 bench.py --gpus 4 > gpurun_out/bench_n4.json 2> gpurun_out/bench_n4.err
+timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29668 bench.py --gpus 2 > gpurun_out/bench_n2.json 2> gpurun_out/bench_n2.err
