@@ -17,7 +17,10 @@ class ReplayLog:
     n_cycles: int = 0
 
 
-def replay_step(ctx, mark_cycle, ptrs, max_cycles: int = 1000, async_stream=None) -> ReplayLog:
+def replay_step(ctx, mark_cycle, ptrs, max_cycles: int = 1000, async_stream=None,
+                drain_after: int = -1) -> ReplayLog:
+    """drain_after >= 0: after that many gr_step cycles (unless the step completed), mark every
+    remaining tensor in schedule order and end the step with one gr_step_drain."""
     by_cycle: dict[int, list[int]] = {}
     for t, m in enumerate(mark_cycle):
         if m >= 0:
@@ -25,6 +28,17 @@ def replay_step(ctx, mark_cycle, ptrs, max_cycles: int = 1000, async_stream=None
     log = ReplayLog()
     c = 0
     while c < max_cycles:
+        if c == drain_after:
+            for cc in sorted(k for k in by_cycle if k >= c):
+                for t in by_cycle[cc]:
+                    if async_stream is None:
+                        ctx.gr_mark_ready(t, ptrs[t])
+                    else:
+                        ctx.gr_mark_ready_async(t, ptrs[t], async_stream)
+            ctx.gr_step_drain()
+            c += 1
+            log.complete = True
+            break
         for t in by_cycle.get(c, []):
             if async_stream is None:
                 ctx.gr_mark_ready(t, ptrs[t])

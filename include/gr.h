@@ -167,6 +167,21 @@ int gr_wait(gr_ctx *ctx);
  * at the next gr_step / gr_wait. With GR_TRACE set it behaves like gr_wait. */
 int gr_wait_async(gr_ctx *ctx);
 
+/* gr_step_drain — COLLECTIVE (every rank calls it at the same cycle, i.e. after the same
+ * number of gr_step calls in this step). The step's final coordination cycle, driven by the
+ * device: every tensor must already be marked on this rank (host marks, or stream-ordered marks
+ * whose flags may still be in flight; otherwise GR_ESTATE and nothing is launched). The
+ * library's coordination stream first waits (stream-ordered, no SM held) for every stream that
+ * issued gr_mark_ready_async in this step; the cycle's bitvector kernel then intersects as
+ * gr_step does (re-checking the marks on the device) and releases every remaining group; the
+ * fused reduction follows as for any cycle. The host does
+ * not wait for the result and the step counts as complete: call gr_wait / gr_wait_async next.
+ * This keeps a training loop's host free to enqueue the next iteration while the tail of
+ * backward and its reduction run (the last tic of a step). A failure on the
+ * device (peer timeout, ABORT, a peer that drained without marking everything) is reported by
+ * the next gr_wait / gr_wait_async / gr_step. */
+int gr_step_drain(gr_ctx *ctx);
+
 /* gr_released_wait_async — LOCAL. Makes `stream` (a cudaStream_t; NULL = world.compute_stream)
  * wait for the reduction of every group released so far in this step, without ending the step
  * or blocking the host: work enqueued on `stream` afterwards sees those groups' reduced

@@ -70,6 +70,7 @@ def _load():
         "gr_wait": ([p], ctypes.c_int),
         "gr_wait_async": ([p], ctypes.c_int),
         "gr_released_wait_async": ([p, p], ctypes.c_int),
+        "gr_step_drain": ([p], ctypes.c_int),
         "gr_set_status": ([p, i32, i32], ctypes.c_int),
         "gr_finalize": ([p], ctypes.c_int),
         "gr_last_error": ([p], ctypes.c_char_p),
@@ -88,7 +89,7 @@ def _load():
 
 
 lib = _load()
-EXPORTED = ("gr_init", "gr_mark_ready", "gr_mark_ready_batch", "gr_mark_ready_async", "gr_step", "gr_wait", "gr_wait_async", "gr_released_wait_async", "gr_set_status",
+EXPORTED = ("gr_init", "gr_mark_ready", "gr_mark_ready_batch", "gr_mark_ready_async", "gr_step", "gr_wait", "gr_wait_async", "gr_released_wait_async", "gr_step_drain", "gr_set_status",
             "gr_finalize", "gr_last_error", "gr_query", "gr_set_timing", "gr_reset_stats", "gr_bench_spin",
             "gr_enable_grad_stats", "gr_grad_stats")
 
@@ -186,6 +187,11 @@ class Context:
 
     def gr_wait_async(self):
         return _check(lib.gr_wait_async(self._ctx), self._ctx)
+
+    def gr_step_drain(self):
+        """Final, device-driven cycle of the step (every tensor already marked); the host does
+        not wait. Follow with gr_wait / gr_wait_async."""
+        return _check(lib.gr_step_drain(self._ctx), self._ctx)
 
     def gr_released_wait_async(self, stream: int = 0):
         """`stream` (a raw cudaStream_t; 0 = the compute stream) waits for every group released

@@ -37,7 +37,7 @@ struct HostResult {
 };
 
 struct HostError {
-    volatile int32_t code;   // 0 none, 3 timeout in the data kernel
+    volatile int32_t code;   // 0 none, 3 timeout in the data kernel, 10 + status: a drain cycle failed
     volatile int32_t where;
 };
 
@@ -82,6 +82,9 @@ struct BvParams {
     uint64_t timeout_ns;
     uint64_t seq;
     int32_t use_inline;
+    int32_t drain;                   // gr_step_drain: wait on the device until every unreleased
+                                     // tensor of this rank is ready, no host hand-off awaited
+    HostError *err;                  // drain only: failures surface here (host-mapped)
     uint32_t inline_bits[GR_BV_INLINE_WORDS];  // snapshot of host_bits passed with the launch
 };
 

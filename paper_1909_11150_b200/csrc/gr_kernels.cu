@@ -118,6 +118,21 @@ __global__ void __launch_bounds__(NT, 1024 / NT) bitvector_kernel(BvParams p) {
             const int lo = (w == 0) ? GR_STATUS_BITS : 0;                 // tensor bits of word w
             const int hi = min(32, p.nbits - w * 32);
             const uint32_t valid = (hi >= 32 ? 0xffffffffu : ((1u << hi) - 1u)) & ~((1u << lo) - 1u);
+            if (p.drain) {  // every unreleased tensor was marked: wait for the stream-ordered flags
+                const uint32_t need = valid & ~sR[w];
+                const int b = w * 32 + lane;
+                const uint64_t dl = globaltimer() + p.timeout_ns;
+                unsigned backoff = 64;
+                while ((ready & need) != need) {
+                    if (globaltimer() > dl) { if (lane == 0) s_timeout = 1; break; }
+                    // the wait can span the whole backward pass: poll gently (exponential
+                    // backoff to ~2 us) so the flag writers' stream memory fences are not slowed
+                    __nanosleep(backoff);
+                    backoff = backoff < 2048 ? 2 * backoff : 2048;
+                    const uint32_t fv = (b >= GR_STATUS_BITS && b < p.nbits) ? ld_relaxed_sys32(p.dev_flags + b) : 0u;
+                    ready = hb[k] | __ballot_sync(0xffffffffu, fv == p.epoch);
+                }
+            }
             uint32_t word = ready & valid & ~sR[w];
             if (w == 0) word |= (p.abort_flag ? 0u : 1u) | (p.shutdown_flag ? 0u : 2u);  // complement-coded (R1)
             if (lane == 0) {
@@ -154,6 +169,7 @@ __global__ void __launch_bounds__(NT, 1024 / NT) bitvector_kernel(BvParams p) {
                 uint64_t x = raw[k][r];
                 while ((uint32_t)(x >> 32) != p.tag) {
                     if (globaltimer() > deadline) { s_timeout = 1; break; }
+                    __nanosleep(64);
                     x = ld_relaxed_sys64(p.slot[r] + (size_t)p.parity * W + w);
                 }
                 a &= (uint32_t)x;
@@ -301,6 +317,12 @@ __global__ void __launch_bounds__(NT, 1024 / NT) bitvector_kernel(BvParams p) {
         p.result->t_anded = t_anded;
         p.result->t_end = globaltimer();
         asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(&p.result->seq), "l"(p.seq) : "memory");
+        // a drain cycle is not awaited by the host: a failure (or a step left incomplete)
+        // is reported through the error block checked by the next gr_step / gr_wait
+        if (p.drain && (status != ST_OK || !complete)) {
+            p.err->where = status;
+            asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(&p.err->code), "r"(10 + status) : "memory");
+        }
     }
 }
 

@@ -78,7 +78,7 @@ struct gr_ctx {
     // device state
     int dev = -1;
     cudaStream_t s_coord = nullptr, s_data = nullptr, s_compute = nullptr;
-    cudaEvent_t ev_compute = nullptr, ev_data_done = nullptr, ev_bv = nullptr, ev_released = nullptr;
+    cudaEvent_t ev_compute = nullptr, ev_data_done = nullptr, ev_bv = nullptr, ev_released = nullptr, ev_drain = nullptr;
     cudaEvent_t ring_ev[GR_SLOT_RING] = {};
     bool ring_pending[GR_SLOT_RING] = {};
     char *symm = nullptr;
@@ -108,10 +108,12 @@ struct gr_ctx {
     gr::HostError *d_err = nullptr;
     size_t res_bytes = 0;
     PFN_writeValue32 write_value32 = nullptr;
-    int data_ctas[4] = {0, 0, 0, 0};
+    int data_ctas[4] = {0, 0, 0, 0};       // world.comm_ctas (or every SM)
+    int data_ctas_full[4] = {0, 0, 0, 0};  // every SM (drain cycles)
     int lag1 = 0, lag2 = 0;  // GR_LAG1 / GR_LAG2 overrides (tuning)
     int nstages = 4, stage_kb = 48;  // GR_STAGES / GR_STAGE_KB overrides (tuning)
     int64_t lc_sub = 8192;           // local kernel sub-item (GR_LC_SUB, tuning)
+    std::vector<void *> async_streams;  // distinct streams of this step's gr_mark_ready_async calls
 
     // step / cycle state
     std::mutex mu;
@@ -174,6 +176,22 @@ int fail(gr_ctx *c, int code, const char *fmt, ...) {
         g_init_error = buf;
     }
     return code;
+}
+
+// an error reported by a kernel through the pinned error block (data-kernel timeout, or a
+// drain cycle that failed / left the step incomplete)
+int device_error(gr_ctx *c) {
+    const int code = c->h_err->code, where = c->h_err->where;
+    if (code == 3)
+        return fail(c, GR_ETIMEOUT, "reduction timed out waiting for a peer (%s flag)", where == 1 ? "pack" : "reduce-scatter");
+    if (code >= 10) {
+        const int st = code - 10;
+        if (st == gr::ST_ABORT) return fail(c, GR_EABORT, "drain cycle: a rank raised ABORT");
+        if (st == gr::ST_SHUTDOWN) return fail(c, GR_ESHUTDOWN, "drain cycle: a rank raised SHUTDOWN");
+        if (st == gr::ST_TIMEOUT) return fail(c, GR_ETIMEOUT, "drain cycle: a mark or a peer's bitvector never arrived");
+        return fail(c, GR_ETIMEOUT, "drain cycle left the step incomplete (a peer drained before marking everything)");
+    }
+    return fail(c, GR_ETIMEOUT, "device error %d", code);
 }
 
 #define RC(expr)              \
@@ -355,6 +373,7 @@ int setup_device(gr_ctx *c) {
     CK(c, cudaEventCreateWithFlags(&c->ev_compute, cudaEventDisableTiming));
     CK(c, cudaEventCreateWithFlags(&c->ev_data_done, cudaEventDisableTiming));
     CK(c, cudaEventCreateWithFlags(&c->ev_released, cudaEventDisableTiming));
+    CK(c, cudaEventCreateWithFlags(&c->ev_drain, cudaEventDisableTiming));
     CK(c, cudaEventCreateWithFlags(&c->ev_bv, cudaEventDisableTiming));
     for (int i = 0; i < GR_SLOT_RING; ++i) CK(c, cudaEventCreateWithFlags(&c->ring_ev[i], cudaEventDisableTiming));
 
@@ -442,6 +461,7 @@ int setup_device(gr_ctx *c) {
         if (rc != 0) return fail(c, GR_ECUDA, "occupancy query failed: %s", cudaGetErrorString((cudaError_t)rc));
         int want = c->world.comm_ctas > 0 ? c->world.comm_ctas : mx;
         c->data_ctas[algo] = std::max(1, std::min(want, mx));
+        c->data_ctas_full[algo] = std::max(1, mx);
     }
     CK(c, cudaDeviceSynchronize());
 
@@ -507,6 +527,7 @@ void free_all(gr_ctx *c) {
     if (c->ev_compute) cudaEventDestroy(c->ev_compute);
     if (c->ev_data_done) cudaEventDestroy(c->ev_data_done);
     if (c->ev_released) cudaEventDestroy(c->ev_released);
+    if (c->ev_drain) cudaEventDestroy(c->ev_drain);
     if (c->ev_bv) cudaEventDestroy(c->ev_bv);
     for (auto &v : {c->pending_data_ev, c->pending_bv_ev, c->free_ev})
         for (auto &pr : v) {
@@ -680,6 +701,8 @@ int gr_mark_ready_async(gr_ctx *c, int32_t rank, int32_t t, void *dev_ptr, void 
     int rc = mark_common(c, rank, t, dev_ptr);
     if (rc) return rc;
     c->async_used = true;
+    if (std::find(c->async_streams.begin(), c->async_streams.end(), stream) == c->async_streams.end())
+        c->async_streams.push_back(stream);
     CUresult r = c->write_value32((CUstream)stream, (CUdeviceptr)(c->d_flags + c->bit_of[t]), c->epoch, 0);
     if (r != CUDA_SUCCESS) {
         c->marked[t] = 0;
@@ -696,12 +719,28 @@ int gr_set_status(gr_ctx *c, int32_t abort_flag, int32_t shutdown_flag) {
     return GR_OK;
 }
 
+static int step_impl(gr_ctx *c, int32_t *released, gr_cycle_info *info, uint32_t *global_bits, bool drain);
+
 int gr_step(gr_ctx *c, int32_t *released, gr_cycle_info *info, uint32_t *global_bits) {
     if (!c || !released) return fail(c, GR_EINVAL, "null argument to gr_step");
+    return step_impl(c, released, info, global_bits, false);
+}
+
+int gr_step_drain(gr_ctx *c) {
+    if (!c) return GR_EINVAL;
+    {
+        std::lock_guard<std::mutex> lk(c->mu);
+        for (int32_t t = 0; t < c->T; ++t)
+            if (!c->marked[t]) return fail(c, GR_ESTATE, "gr_step_drain: tensor %d is not marked in this step", t);
+    }
+    return step_impl(c, nullptr, nullptr, nullptr, true);
+}
+
+static int step_impl(gr_ctx *c, int32_t *released, gr_cycle_info *info, uint32_t *global_bits, bool drain) {
     if (c->dry) return fail(c, GR_ESTATE, "dry context (device < 0) cannot step");
     if (c->sticky) return fail(c, GR_ESTATE, "context is in a sticky error state (%d): %s", c->sticky, c->err.c_str());
     const auto h_enter = std::chrono::steady_clock::now();
-    if (c->h_err->code) return fail(c, GR_ETIMEOUT, "a previous reduction timed out waiting for a peer");
+    if (c->h_err->code) return device_error(c);
     CK(c, cudaSetDevice(c->dev));
     const int slot = (int)(c->cycle % GR_SLOT_RING);
     if (c->ring_pending[slot]) {  // the data launch that read this slot must be done
@@ -766,12 +805,28 @@ int gr_step(gr_ctx *c, int32_t *released, gr_cycle_info *info, uint32_t *global_
     p.timeout_ns = (uint64_t)c->world.timeout_ms * 1000000ull;
     p.seq = ++c->seq;
     p.use_inline = p_inline;
+    p.drain = drain ? 1 : 0;
+    p.err = c->h_err;
     if (p_inline) memcpy(p.inline_bits, inline_bits, sizeof(uint32_t) * c->W);
 
     std::pair<cudaEvent_t, cudaEvent_t> evb{};
     if (c->timing) {
         evb = get_ev_pair(c);
         CK(c, cudaEventRecord(evb.first, c->s_coord));
+    }
+    if (drain) {
+        // the drain kernel must not sit on an SM for the rest of backward (it would displace
+        // compute, e.g. a persistent GEMM's last CTA): the coordination stream itself waits,
+        // in the stream front end, for every stream that issued stream-ordered marks
+        std::vector<void *> streams;
+        {
+            std::lock_guard<std::mutex> lk(c->mu);
+            streams = c->async_streams;
+        }
+        for (void *ms : streams) {
+            CK(c, cudaEventRecord(c->ev_drain, static_cast<cudaStream_t>(ms)));
+            CK(c, cudaStreamWaitEvent(c->s_coord, c->ev_drain, 0));
+        }
     }
     if (!p_inline)  // larger bitvectors: one DMA of the pinned mark bits, stream-ordered before the kernel
         CK(c, cudaMemcpyAsync(c->d_hbits_dev, c->h_bits, sizeof(uint32_t) * c->W, cudaMemcpyHostToDevice, c->s_coord));
@@ -834,7 +889,9 @@ int gr_step(gr_ctx *c, int32_t *released, gr_cycle_info *info, uint32_t *global_
         d.inv_n = 1.0f / (float)c->N;
         d.timeout_ns = (uint64_t)c->world.timeout_ms * 1000000ull;
         const bool local = c->N == 1;
-        const int ctas = c->data_ctas[local ? gr::ALGO_LOCAL : gr::ALGO_TWOSHOT];
+        // a drain cycle's reduction starts when backward is over: it gets every SM
+        const int ctas = drain ? c->data_ctas_full[local ? gr::ALGO_LOCAL : gr::ALGO_TWOSHOT]
+                               : c->data_ctas[local ? gr::ALGO_LOCAL : gr::ALGO_TWOSHOT];
         d.lc_sub = c->lc_sub;
         d.lag1 = c->lag1 > 0 ? c->lag1 : 2 * ctas;
         d.lag2 = c->lag2 > 0 ? c->lag2 : 4 * ctas;
@@ -867,6 +924,14 @@ int gr_step(gr_ctx *c, int32_t *released, gr_cycle_info *info, uint32_t *global_
         CK(c, cudaEventRecord(c->ring_ev[slot], c->s_data));
         c->ring_pending[slot] = true;
         c->stats.data_launches++;
+    }
+
+    if (drain) {  // device-driven final cycle: the host does not wait for the hand-off
+        c->cycle++;
+        c->stats.cycles++;
+        std::lock_guard<std::mutex> lk(c->mu);
+        c->step_complete = true;
+        return GR_OK;
     }
 
     // wait for the kernel's hand-off (pinned host memory), bounded
@@ -962,6 +1027,7 @@ static int start_next_step(gr_ctx *c) {
         memset(c->h_bits, 0, sizeof(uint32_t) * (size_t)c->W);  // no bitvector kernel is in flight
         c->step_fresh = true;
         c->async_used = false;
+        c->async_streams.clear();
     }
     return GR_OK;
 }
@@ -971,7 +1037,7 @@ int gr_wait_async(gr_ctx *c) {
     if (!c->trace_path.empty()) return gr_wait(c);
     if (c->dry) return fail(c, GR_ESTATE, "dry context (device < 0) cannot wait");
     if (c->sticky == GR_ECUDA) return fail(c, GR_ESTATE, "context is in a sticky error state: %s", c->err.c_str());
-    if (c->h_err->code) return fail(c, GR_ETIMEOUT, "reduction timed out waiting for a peer");
+    if (c->h_err->code) return device_error(c);
     CK(c, cudaSetDevice(c->dev));
     CK(c, cudaEventRecord(c->ev_data_done, c->s_data));
     CK(c, cudaStreamWaitEvent(c->s_compute, c->ev_data_done, 0));
@@ -996,10 +1062,7 @@ int gr_wait(gr_ctx *c) {
     CK(c, cudaSetDevice(c->dev));
     CK(c, cudaStreamSynchronize(c->s_coord));
     CK(c, cudaStreamSynchronize(c->s_data));
-    if (c->h_err->code) {
-        const int where = c->h_err->where;
-        return fail(c, GR_ETIMEOUT, "reduction timed out waiting for a peer (%s flag)", where == 1 ? "pack" : "reduce-scatter");
-    }
+    if (c->h_err->code) return device_error(c);
     CK(c, cudaEventRecord(c->ev_data_done, c->s_data));
     CK(c, cudaStreamWaitEvent(c->s_compute, c->ev_data_done, 0));
     for (int i = 0; i < GR_SLOT_RING; ++i) c->ring_pending[i] = false;

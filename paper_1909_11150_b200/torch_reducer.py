@@ -44,6 +44,12 @@ def contiguous_groups(numels, n_groups: int):
 
 
 class GroupedGradReducer:
+    """comm_ctas bounds the SMs a reduction occupies while backward is still running (0 = every
+    SM; the fused kernel holds a large shared-memory ring, so each of its CTAs displaces compute
+    on its SM); the step's final, device-driven cycle (gr_step_drain) always uses every SM.
+    Defaults are the best measured on a 51M-parameter FC-DenseNet at N=2/4 (tools/bench_train.py,
+    DESIGN.md §11): 4 groups, full grid, drain of the last group."""
+
     def __init__(self, params, *, rank: int, world_size: int, device: int, groups=None, n_groups: int = 4,
                  buffer_dtype: int = GR_F16, pg=None, timeout_ms: int = 0, comm_ctas: int = 0):
         self.params = [p for p in params if p.requires_grad]
@@ -59,29 +65,71 @@ class GroupedGradReducer:
                            compute_stream=torch.cuda.current_stream(device).cuda_stream, timeout_ms=timeout_ms,
                            comm_ctas=comm_ctas, allgather=self._ag)
         self.cycles_last_step = 0
+        self.G = len(set(self.group_of))
+        self._gsize = [0] * self.G
+        for g in self.group_of:
+            self._gsize[g] += 1
+        self._left = list(self._gsize)
+        self._ready_order = []  # groups in the order their last gradient was produced (host view)
+        self._events = [torch.cuda.Event() for _ in range(self.G)]
         self._hooks = [p.register_post_accumulate_grad_hook(self._make_hook(t)) for t, p in enumerate(self.params)]
 
     def _make_hook(self, t: int):
+        g = self.group_of[t]
+
         def hook(p):
             # stream-ordered readiness: the flag is written after the accumulation kernel
-            self.ctx.gr_mark_ready_async(t, p.grad.data_ptr(), torch.cuda.current_stream(p.device).cuda_stream)
+            stream = torch.cuda.current_stream(p.device)
+            self.ctx.gr_mark_ready_async(t, p.grad.data_ptr(), stream.cuda_stream)
+            self._left[g] -= 1
+            if self._left[g] == 0:  # the group's last gradient: an event tells the host when
+                self._events[g].record(stream)
+                self._ready_order.append(g)
         return hook
 
-    def synchronize(self, cycle_us: float = 0.0, max_cycles: int = 1_000_000):
-        """Run coordination cycles until the step's gradients are all released, then order the
-        current stream after their reduction. Returns the number of cycles."""
-        n = 0
-        nxt = time.perf_counter()
-        while n < max_cycles:
-            _rel, complete, _bits, _info = self.ctx.gr_step()
-            n += 1
-            if complete:
-                break
-            if cycle_us > 0:
+    def synchronize(self, cycle_us: float = 0.0, drain_tail: int = 1, max_cycles: int = 1_000_000):
+        """Coordinate the step's reduction while backward is still running on the GPU.
+
+        Cycles are driven by local readiness: for each group, in the order its last gradient
+        was produced, the host waits on a CUDA event recorded after that gradient and then runs
+        cycles until the group is released (a peer that is behind holds the cycle on the device
+        only for the skew). Once at most `drain_tail` groups are left, a device-driven drain
+        cycle (gr_step_drain) ends the step without the host waiting for the tail of backward.
+        `cycle_us` > 0 instead polls with fixed-period cycles (the paper's cycle time).
+        Returns the number of cycles."""
+        n, complete = 0, False
+        released = set()
+        if cycle_us > 0:
+            nxt = time.perf_counter()
+            while n < max_cycles and self.G - len(released) > drain_tail:
+                rel, complete, _bits, _info = self.ctx.gr_step()
+                n += 1
+                released.update(rel)
+                if complete:
+                    break
                 nxt += cycle_us * 1e-6
                 while time.perf_counter() < nxt:
                     pass
+        else:
+            for g in self._ready_order:
+                if complete or self.G - len(released) <= drain_tail or n >= max_cycles:
+                    break
+                if g in released:
+                    continue
+                self._events[g].synchronize()  # the group's gradients exist on this rank
+                while g not in released and n < max_cycles:
+                    rel, complete, _bits, _info = self.ctx.gr_step()
+                    n += 1
+                    released.update(rel)
+                    # decided on the global released set only: every rank leaves at the same cycle
+                    if complete or self.G - len(released) <= drain_tail:
+                        break
+        if not complete:
+            self.ctx.gr_step_drain()  # every hook has fired: all marks are issued
+            n += 1
         self.ctx.gr_wait_async()
+        self._left = list(self._gsize)
+        self._ready_order = []
         self.cycles_last_step = n
         return n
 

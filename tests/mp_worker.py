@@ -176,6 +176,28 @@ def main():
                     gf = (rng.random(T) < 0.3).tolist()
                     for osm in (0, 1 << 62):
                         run(case, seed, buf, grad_f16=gf, osm=osm, stats=True)
+            elif args.suite == "drain":
+                from tests.parity_lib import run_drain_case_on_rank
+                stream = torch.cuda.Stream(device=dev)
+                for seed in range(s0, s1):
+                    case = cfg1_case(seed, N=N)
+                    ncase += 1
+                    ctx = Context(rank=rank, world_size=N, device=local, numel=case.numel, group_of=case.group_of,
+                                  buffer_dtype=GR_F16 if buf == "f16" else GR_F32, timeout_ms=20000, allgather=ag)
+                    ok = True
+                    try:
+                        _log, h = run_drain_case_on_rank(ctx, case, rank, seed, dev, buf == "f16", seed % 3,
+                                                         async_stream=stream.cuda_stream if seed % 2 else None)
+                    except AssertionError as e:
+                        ok, h = False, "FAIL"
+                        print(f"[rank {rank}] drain seed {seed} buf {buf}: {e}", flush=True)
+                    hs = [None] * N
+                    dist.all_gather_object(hs, h)
+                    if ok and len(set(hs)) != 1:
+                        ok = False
+                        print(f"[rank {rank}] drain seed {seed}: outputs differ across ranks", flush=True)
+                    failures += (not ok)
+                    ctx.gr_finalize()
             elif args.suite == "autograd":
                 ncase += 1
                 ok = autograd_suite(rank, N, local, dev)

@@ -122,3 +122,26 @@ def check_grad_stats(ctx, case, seed, buffer_f16: bool, grad_f16=None, kind="uni
             tol = 2.0 ** -9 * want + 1e-30
         assert abs(sumsq[t] - want) <= tol, f"{where}: tensor {t} sumsq gpu={sumsq[t]!r} oracle={want!r}"
     return sumsq
+
+
+def run_drain_case_on_rank(ctx, case, r, seed, device, buffer_f16: bool, drain_after: int, async_stream=None):
+    """gr_step_drain: the first `drain_after` cycles follow the oracle's schedule exactly; the
+    drain cycle then releases every remaining group, so every tensor ends up reduced — values
+    bit-exact against the oracle's emulation (they do not depend on the schedule, R5)."""
+    import torch
+
+    grads = make_grads(case.numel, r, seed, device)
+    torch.cuda.synchronize(device)
+    log = replay_step(ctx, case.mark_cycle[r], [g.data_ptr() for g in grads], 1000,
+                      async_stream=async_stream, drain_after=drain_after)
+    ref = oracle.simulate_step(case.N, case.group_of, case.mark_cycle, max_cycles=1000)
+    k = len(log.released)
+    assert log.released == ref.released[:k], f"rank {r} seed {seed}: pre-drain schedule {log.released} != {ref.released[:k]}"
+    h = hashlib.sha256()
+    for t in range(case.T):
+        out = grads[t].float().cpu().numpy()
+        h.update(out.tobytes())
+        idx = sample_indices(out.size, seed * 7919 + t)
+        gs = host_inputs(case.numel, case.N, seed, t, False, "uniform", idx)
+        check_values(out[idx], gs, case.N, buffer_f16, False, where=f"rank {r} seed {seed} tensor {t} (drain)")
+    return log, h.hexdigest()

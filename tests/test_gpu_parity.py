@@ -229,6 +229,43 @@ def test_released_wait_async_orders_copy_out(gpu):
     ctx.gr_finalize()
 
 
+@pytest.mark.parametrize("buf16", [True, False])
+def test_step_drain_n1(gpu, buf16):
+    """gr_step_drain: the cycles before it follow the oracle's schedule, the drain cycle releases
+    every remaining group; values bit-exact. With stream-ordered marks queued behind 50 ms of
+    device work the call returns at once and the device waits for the marks."""
+    import torch
+    from paper_1909_11150_b200 import gr_bench_spin
+    from tests.parity_lib import run_drain_case_on_rank
+    for seed in range(12):
+        case = _n1(cfg1_case(seed))
+        ctx = _ctx(case, buf16)
+        run_drain_case_on_rank(ctx, case, 0, seed, gpu, buf16, drain_after=seed % 3)
+        ctx.gr_finalize()
+    case = _n1(cfg1_case(99))
+    ctx = _ctx(case, buf16)
+    s = torch.cuda.Stream(device=gpu)
+    gr_bench_spin(50_000_000, 4, s.cuda_stream)
+    run_drain_case_on_rank(ctx, case, 0, 99, gpu, buf16, drain_after=0, async_stream=s.cuda_stream)
+    ctx.gr_finalize()
+
+
+def test_step_drain_requires_every_mark(gpu):
+    import torch
+    from paper_1909_11150_b200 import GR_F16, Context, GrError
+    from paper_1909_11150_b200.binding import GR_ESTATE
+    x = torch.zeros(64, device=gpu)
+    ctx = Context(rank=0, world_size=1, device=0, numel=[64, 64], group_of=[0, 1], buffer_dtype=GR_F16)
+    ctx.gr_mark_ready(0, x.data_ptr())
+    with pytest.raises(GrError) as e:
+        ctx.gr_step_drain()
+    assert e.value.code == GR_ESTATE
+    ctx.gr_mark_ready(1, x.data_ptr())
+    ctx.gr_step_drain()
+    ctx.gr_wait()
+    ctx.gr_finalize()
+
+
 def test_fcn220m_n1_full_size(gpu):
     """The bench workload at full size (225,115,137 elements, 68 tensors,
     10 groups), reverse-layer schedule; values checked on sampled elements."""
@@ -282,6 +319,14 @@ def test_multi_gpu_nvls(n):
         pytest.skip(f"needs {n} GPUs")
     assert _torchrun(n, "--suite", "edge", "--seeds", "0:3", env_extra={"GR_NVLS": "1"}) == 0
     assert _torchrun(n, "--suite", "fcn", "--seeds", "7:8", env_extra={"GR_NVLS": "1"}) == 0
+
+
+@pytest.mark.parametrize("n", [2, 4, 8])
+def test_multi_gpu_step_drain(n):
+    """gr_step_drain across ranks: host and stream-ordered marks, drain after 0-2 cycles."""
+    if gpu_count() < n:
+        pytest.skip(f"needs {n} GPUs")
+    assert _torchrun(n, "--suite", "drain", "--seeds", "0:12") == 0
 
 
 @pytest.mark.parametrize("n", [2, 4, 8])
