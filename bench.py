@@ -464,15 +464,21 @@ def run_extras(args, ctx, grads, ptrs, tensor_order, f, N, rank, local, dev, com
             ctx2.gr_mark_ready_async(2 * l, ptrs[2 * l], compute.cuda_stream)
             ctx2.gr_mark_ready_async(2 * l + 1, ptrs[2 * l + 1], compute.cuda_stream)
         ev_bwd.record(compute)
-        # cycle loop: one gr_step per tic until every group has been released
+        # cycle loop: one gr_step per tic while backward runs; once only the last group is
+        # pending, one device-driven drain cycle (gr_step_drain) releases it the moment its
+        # marks land, without waiting for the next tic or a host round trip
         nxt = time.perf_counter()
-        while True:
-            _rel, complete, _A, _ = ctx2.gr_step()
+        left, complete = f.G, False
+        while left > 1:
+            rel, complete, _A, _ = ctx2.gr_step()
+            left -= len(rel)
             if complete:
                 break
             nxt += cyc
             while time.perf_counter() < nxt:
                 pass
+        if not complete:
+            ctx2.gr_step_drain()
         ctx2.gr_wait()
         ev_end.record(compute)
         torch.cuda.synchronize()
@@ -493,7 +499,8 @@ def run_extras(args, ctx, grads, ptrs, tensor_order, f, N, rank, local, dev, com
                            "frac_of_bwd": round(float(np.mean(ex_max)) / float(np.mean(bwd)), 5),
                            "cycle_us": args.cycle_us, "comm_sms": comm_sms, "steps": len(exposed),
                            "compute": "gr_bench_spin per layer, d_l=2*OPS_l/(0.70*1401.8 TF/s) x U(0.9,1.1)",
-                           "marks": "gr_mark_ready_async on the compute stream after each layer"}
+                           "marks": "gr_mark_ready_async on the compute stream after each layer",
+                           "cycles": "host tics while backward runs; the last group by gr_step_drain"}
     ctx2.gr_finalize()
 
     # ---- NEXT-2 epilogue cost: the same step with the fused ||g||^2 / non-finite statistics ----

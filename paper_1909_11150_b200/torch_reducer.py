@@ -43,6 +43,55 @@ def contiguous_groups(numels, n_groups: int):
     return [remap[v] for v in gid]
 
 
+def drive_cycles(step, drain, wait_group, ready_order, G: int, drain_tail: int = 1, cycle_us: float = 0.0,
+                 max_cycles: int = 1_000_000) -> int:
+    """The host side of one step's coordination (argument marshalling around gr_step).
+
+    Cycles are driven by local readiness: for each group, in the order its last gradient was
+    produced on this rank (`ready_order`), wait_group(g) blocks until it exists, then cycles run
+    until g is released (a peer that is behind holds the cycle on the device only for the skew).
+    Once at most `drain_tail` groups are left, drain() (gr_step_drain) ends the step without the
+    host waiting for the tail of backward. `cycle_us` > 0 polls with fixed-period cycles instead
+    (the paper's cycle time).
+
+    Every decision to cycle, stop or drain depends only on the released set, which the global
+    AND makes identical on every rank, so all ranks issue the same sequence of collective calls
+    whatever their local readiness order (tests/test_torch_reducer.py). Returns the cycles run."""
+    n, complete = 0, False
+    released = set()
+
+    def cycle():
+        nonlocal n, complete
+        rel, complete = step()
+        n += 1
+        released.update(rel)
+
+    if cycle_us > 0:
+        nxt = time.perf_counter()
+        while n < max_cycles and G - len(released) > drain_tail:
+            cycle()
+            if complete:
+                break
+            nxt += cycle_us * 1e-6
+            while time.perf_counter() < nxt:
+                pass
+    else:
+        for g in ready_order:
+            if complete or G - len(released) <= drain_tail or n >= max_cycles:
+                break
+            if g in released:
+                continue
+            wait_group(g)  # the group's gradients exist on this rank
+            while g not in released and n < max_cycles:
+                cycle()
+                if complete or G - len(released) <= drain_tail:
+                    break
+    if not complete:
+        drain()  # every hook has fired: all marks are issued
+        n += 1
+    return n
+
+
 class GroupedGradReducer:
     """comm_ctas bounds the SMs a reduction occupies while backward is still running (0 = every
     SM; the fused kernel holds a large shared-memory ring, so each of its CTAs displaces compute
@@ -88,45 +137,14 @@ class GroupedGradReducer:
         return hook
 
     def synchronize(self, cycle_us: float = 0.0, drain_tail: int = 1, max_cycles: int = 1_000_000):
-        """Coordinate the step's reduction while backward is still running on the GPU.
+        """Coordinate the step's reduction while backward is still running on the GPU
+        (see drive_cycles), then order the current stream after it. Returns the cycles run."""
+        def step():
+            rel, complete, _bits, _info = self.ctx.gr_step()
+            return rel, complete
 
-        Cycles are driven by local readiness: for each group, in the order its last gradient
-        was produced, the host waits on a CUDA event recorded after that gradient and then runs
-        cycles until the group is released (a peer that is behind holds the cycle on the device
-        only for the skew). Once at most `drain_tail` groups are left, a device-driven drain
-        cycle (gr_step_drain) ends the step without the host waiting for the tail of backward.
-        `cycle_us` > 0 instead polls with fixed-period cycles (the paper's cycle time).
-        Returns the number of cycles."""
-        n, complete = 0, False
-        released = set()
-        if cycle_us > 0:
-            nxt = time.perf_counter()
-            while n < max_cycles and self.G - len(released) > drain_tail:
-                rel, complete, _bits, _info = self.ctx.gr_step()
-                n += 1
-                released.update(rel)
-                if complete:
-                    break
-                nxt += cycle_us * 1e-6
-                while time.perf_counter() < nxt:
-                    pass
-        else:
-            for g in self._ready_order:
-                if complete or self.G - len(released) <= drain_tail or n >= max_cycles:
-                    break
-                if g in released:
-                    continue
-                self._events[g].synchronize()  # the group's gradients exist on this rank
-                while g not in released and n < max_cycles:
-                    rel, complete, _bits, _info = self.ctx.gr_step()
-                    n += 1
-                    released.update(rel)
-                    # decided on the global released set only: every rank leaves at the same cycle
-                    if complete or self.G - len(released) <= drain_tail:
-                        break
-        if not complete:
-            self.ctx.gr_step_drain()  # every hook has fired: all marks are issued
-            n += 1
+        n = drive_cycles(step, self.ctx.gr_step_drain, lambda g: self._events[g].synchronize(),
+                         self._ready_order, self.G, drain_tail, cycle_us, max_cycles)
         self.ctx.gr_wait_async()
         self._left = list(self._gsize)
         self._ready_order = []
