@@ -45,6 +45,7 @@ bool entry(const char *name, F &fn) {
 struct Api {
     CUresult (*DeviceGet)(CUdevice *, int);
     CUresult (*DeviceGetAttribute)(int *, CUdevice_attribute, CUdevice);
+    CUresult (*DeviceGetUuid)(CUuuid *, CUdevice);
     CUresult (*MulticastGetGranularity)(size_t *, const CUmulticastObjectProp *, CUmulticastGranularity_flags);
     CUresult (*MulticastCreate)(CUmemGenericAllocationHandle *, const CUmulticastObjectProp *);
     CUresult (*MulticastAddDevice)(CUmemGenericAllocationHandle, CUdevice);
@@ -64,6 +65,7 @@ struct Api {
 
     bool load() {
         return entry("cuDeviceGet", DeviceGet) && entry("cuDeviceGetAttribute", DeviceGetAttribute) &&
+               entry("cuDeviceGetUuid", DeviceGetUuid) &&
                entry("cuMulticastGetGranularity", MulticastGetGranularity) &&
                entry("cuMulticastCreate", MulticastCreate) && entry("cuMulticastAddDevice", MulticastAddDevice) &&
                entry("cuMulticastBindMem", MulticastBindMem) && entry("cuMulticastUnbind", MulticastUnbind) &&
@@ -183,6 +185,19 @@ int nvls_setup(Nvls &s, int rank, int N, int dev, size_t bytes,
     if (!vote(ag, N, ok)) {
         why = "multicast not supported on every rank";
         return 1;
+    }
+    {   // one multicast member per device: ranks sharing a GPU (oversubscribed tests) cannot use it
+        CUuuid id{};
+        ok = g_api.DeviceGetUuid(&id, cudev) == CUDA_SUCCESS;
+        std::vector<CUuuid> ids(N);
+        if (ag(&id, ids.data(), sizeof(CUuuid)) != 0) ok = false;
+        for (int i = 0; ok && i < N; ++i)
+            for (int j = i + 1; ok && j < N; ++j)
+                if (memcmp(&ids[i], &ids[j], sizeof(CUuuid)) == 0) ok = false;
+        if (!vote(ag, N, ok)) {
+            why = "ranks share a device (or no device UUID)";
+            return 1;
+        }
     }
     s.cudev = cudev;
     CUmulticastObjectProp mp{};

@@ -101,7 +101,9 @@ def main():
 
     rank = int(os.environ["RANK"])
     N = int(os.environ["WORLD_SIZE"])
-    local = int(os.environ.get("LOCAL_RANK", rank))
+    # more ranks than GPUs (the N=8 path on a 4-GPU box): ranks share devices round-robin; the
+    # processes then time-slice each GPU, which is slow but exercises every N-rank code path
+    local = int(os.environ.get("LOCAL_RANK", rank)) % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     dist.init_process_group("gloo")
     ag = make_allgather(None)
