@@ -1,1 +1,1 @@
-timeout 1700 python -m pytest tests/test_gpu_parity.py -q -x -k "oversubscribed" -s > gpurun_out/pt_os.log 2>&1; tail -30 gpurun_out/pt_os.log
+bash tools/sweep.sh 4 "GR_NVLS=0" "GR_NVLS=1" "GR_NVLS=1 GR_CHUNK_DIV=148" > gpurun_out/sw_nvls3.txt 2>&1
