@@ -771,7 +771,7 @@ __device__ __forceinline__ void xf_consume(const DataParams &p, const XfMeta &m,
             const int64_t e = 8 * v, bi = pc.lo + e, ti = pc.toff + e;
             const int64_t so = (bi - sb) * B::ES;  // byte offset inside a peer slot
             float acc[8];
-            if constexpr (KIND == K_PACK) {
+            if constexpr (KIND == K_PACK) {  // own_buf: this rank's buffer, or (push) the owner's slot
                 lds_grad8(gs + e * esz, pc.f16, acc);
                 B::store(own_buf, bi, B::from_f32(acc));
                 continue;
@@ -796,7 +796,15 @@ __device__ __forceinline__ void xf_consume(const DataParams &p, const XfMeta &m,
 #pragma unroll
                 for (int i = 0; i < 8; ++i) acc[i] = acc[i] * p.inv_n;
                 typename B::Raw out = B::from_f32(acc);
-                if constexpr (KIND == K_RS) B::store(own_buf, bi, out);
+                if constexpr (KIND == K_RS) {
+                    if (p.push) {  // push the reduced chunk into every peer's buffer
+#pragma unroll
+                        for (int q = 0; q < GR_MAX_RANKS; ++q)
+                            if (q < p.N && q != p.rank) B::store(p.buf[q], bi, out);
+                    } else {
+                        B::store(own_buf, bi, out);
+                    }
+                }
             }
             grad_store(pc.g, ti, pc.f16, acc);
             if (STATS) st.add8(acc, pc.f16);
@@ -822,7 +830,14 @@ __device__ __forceinline__ void xf_consume(const DataParams &p, const XfMeta &m,
                     a = (r == 0) ? x : a + x;
                 }
                 y = B::round1(a * p.inv_n);
-                if constexpr (KIND == K_RS) B::store1(own_buf, bi, y);
+                if constexpr (KIND == K_RS) {
+                    if (p.push) {
+                        for (int q = 0; q < p.N; ++q)
+                            if (q != p.rank) B::store1(p.buf[q], bi, y);
+                    } else {
+                        B::store1(own_buf, bi, y);
+                    }
+                }
             }
             grad_store1(pc.g, ti, pc.f16, y);
             if (STATS) st.add1(y, pc.f16);
@@ -950,6 +965,7 @@ __global__ void __maxnreg__(96) xfer_kernel(DataParams p) {
         const long long prof_t0 = clock64();
         // stream chunk c as sub-tiles of `sub` elements. src: 0 none (PACK), 1 every peer
         // (RED/RS), 2 the owner (AG); grads: stage own gradient pieces (PACK/RED/RS)
+        const bool pushed = p.push && ALGO == ALGO_TWOSHOT;
         auto produce = [&](int kind, int item, int c, int64_t sub, int src, int owner, bool grads) {
             const Chunk ch = p.chunks[c];
             const int nseg = ch.seg_end - ch.seg_begin;
@@ -1017,7 +1033,11 @@ __global__ void __maxnreg__(96) xfer_kernel(DataParams p) {
                     const bool mine = src == 1 ? (lane < p.N && lane != p.rank) : (src == 2 ? lane == owner : lane == 0);
                     if (mine) {
                         const int slot = (src == 1) ? (lane < p.rank ? lane : lane - 1) : 0;
-                        const char *from = (src == 3) ? p.nvls_uc : p.buf[lane];  // 3: own NVLS copy
+                        // 3: own NVLS copy; push two-shot: RS reads the local receive slot of
+                        // source `lane`, AG the own buffer (the owner pushed into it)
+                        const char *from = (src == 3) ? p.nvls_uc
+                                           : !pushed ? p.buf[lane]
+                                           : (src == 1 ? p.rsb[p.rank] + (size_t)slot * p.rsb_stride : p.buf[p.rank]);
                         mbar_expect_tx(bar, bytes);
                         bulk_g2s(dst + (size_t)slot * p.slot_bytes_red, from + sb * B::ES, bytes, bar);
                     }
@@ -1158,7 +1178,14 @@ __global__ void __maxnreg__(96) xfer_kernel(DataParams p) {
             const int item = m.item, c = m.chunk, last = m.last;
             const char *st = xsm + (size_t)stage * stage_bytes;
             char *own = ALGO == ALGO_NVLS ? p.nvls_uc : p.buf[p.rank];  // this rank's fusion buffer
-            if (kind == K_PACK) xf_consume<BT, K_PACK, STATS>(p, m, st, 0, st, ct, own);
+            if (kind == K_PACK) {
+                char *dst = own;  // push two-shot: straight into the owner's receive slot (NVLink)
+                if (ALGO == ALGO_TWOSHOT && p.push) {
+                    const int o = c % p.N;
+                    dst = p.rsb[o] + (size_t)(p.rank < o ? p.rank : p.rank - 1) * p.rsb_stride;
+                }
+                xf_consume<BT, K_PACK, STATS>(p, m, st, 0, st, ct, dst);
+            }
             else if (kind == K_RED) xf_consume<BT, K_RED, STATS>(p, m, st, p.slot_bytes_red, st + gslot_off, ct, own);
             else if (kind == K_RS) xf_consume<BT, K_RS, STATS>(p, m, st, p.slot_bytes_red, st + gslot_off, ct, own);
             else if (kind == K_NRS) xf_nvls_reduce<BT, STATS>(p, m, ct);

@@ -84,6 +84,8 @@ struct gr_ctx {
     char *symm = nullptr;
     size_t symm_bytes = 0, off_slot = 0, off_pad = 0, off_buf = 0, pad_parity_u32 = 0;
     size_t buf_parity_bytes = 0;
+    size_t off_rsb = 0, rsb_parity_bytes = 0;  // push two-shot receive slots (N-1 buffers per parity)
+    bool push = false;                           // GR_PUSH=1: push two-shot (measured slower)
     char *peer_symm[GR_MAX_RANKS] = {};
     Seg *d_segs = nullptr;
     Chunk *d_chunks = nullptr;
@@ -336,6 +338,9 @@ int build_layouts(gr_ctx *c, const gr_tensor *table, const int32_t *group_of) {
     h = fnv1a(h, &c->buf_f16, sizeof c->buf_f16);
     h = fnv1a(h, &c->chunk_elems, sizeof c->chunk_elems);
     h = fnv1a(h, &c->one_shot_max_bytes, sizeof c->one_shot_max_bytes);
+    h = fnv1a(h, &c->push, sizeof c->push);
+    h = fnv1a(h, &c->chunk_target_div, sizeof c->chunk_target_div);
+    h = fnv1a(h, &c->chunk_max, sizeof c->chunk_max);
     h = fnv1a(h, c->numel.data(), sizeof(int64_t) * T);
     h = fnv1a(h, c->grad_f16.data(), sizeof(int32_t) * T);
     h = fnv1a(h, c->group_of.data(), sizeof(int32_t) * T);
@@ -384,7 +389,9 @@ int setup_device(gr_ctx *c) {
     c->pad_parity_u32 = (size_t)c->C * c->N + c->C;
     c->off_buf = align_up(c->off_pad + sizeof(uint32_t) * 2 * c->pad_parity_u32, kAlign);
     c->buf_parity_bytes = (c->N > 1) ? align_up((size_t)c->buf_elems * esz, kAlign) : 0;
-    c->symm_bytes = c->off_buf + 2 * c->buf_parity_bytes;
+    c->off_rsb = c->off_buf + 2 * c->buf_parity_bytes;
+    c->rsb_parity_bytes = (c->N > 1 && c->push) ? (size_t)(c->N - 1) * c->buf_parity_bytes : 0;
+    c->symm_bytes = c->off_rsb + 2 * c->rsb_parity_bytes;
     cudaError_t e = cudaMalloc((void **)&c->symm, c->symm_bytes);
     if (e != cudaSuccess) return fail(c, GR_ENOMEM, "cudaMalloc(%zu) of symmetric memory: %s", c->symm_bytes, cudaGetErrorString(e));
     CK(c, cudaMemset(c->symm, 0, c->off_buf));
@@ -591,6 +598,7 @@ int gr_init(gr_ctx **out, const gr_world *world, const gr_tensor *table, int32_t
     c->buf_f16 = world->buffer_dtype == GR_F16;
     c->chunk_elems = world->chunk_elems;  // 0: adaptive per group (build_layouts)
     if (const char *ls = getenv("GR_LC_SUB")) c->lc_sub = std::max<int64_t>(256, atoll(ls) / 8 * 8);  // tuning
+    if (const char *pu = getenv("GR_PUSH")) c->push = atoi(pu) != 0;  // tuning / comparison
     if (const char *cd = getenv("GR_CHUNK_DIV")) c->chunk_target_div = std::max<int64_t>(1, atoll(cd));  // tuning
     if (const char *cm = getenv("GR_CHUNK_MAX")) c->chunk_max = std::max<int64_t>(8192, atoll(cm));      // tuning
     if (world->chunk_elems == 0)
@@ -858,6 +866,7 @@ static int step_impl(gr_ctx *c, int32_t *released, gr_cycle_info *info, uint32_t
         for (int r = 0; r < c->N; ++r) {
             char *base = c->peer_symm[r];
             d.buf[r] = base + c->off_buf + (size_t)par * c->buf_parity_bytes;
+            d.rsb[r] = c->push ? base + c->off_rsb + (size_t)par * c->rsb_parity_bytes : nullptr;
             uint32_t *pad = reinterpret_cast<uint32_t *>(base + c->off_pad) + (size_t)par * c->pad_parity_u32;
             d.pack_flag[r] = pad;
             d.rs_flag[r] = pad + (size_t)c->C * c->N;
@@ -883,6 +892,8 @@ static int step_impl(gr_ctx *c, int32_t *released, gr_cycle_info *info, uint32_t
         d.sub_pack = std::max<int64_t>(256, std::min<int64_t>(stage / 4 / 256 * 256, cmax));
         d.sub_ag = std::max<int64_t>(256, std::min<int64_t>(stage / es / 256 * 256, cmax));
         d.one_shot_max_bytes = c->one_shot_max_bytes;
+        d.push = c->push ? 1 : 0;
+        d.rsb_stride = (int64_t)c->buf_parity_bytes;
         d.rank = c->rank;
         d.N = c->N;
         d.epoch = epoch;
