@@ -301,6 +301,8 @@ def test_multi_gpu_edge(n):
     if gpu_count() < n:
         pytest.skip(f"needs {n} GPUs")
     assert _torchrun(n, "--suite", "edge", "--seeds", "0:4") == 0
+    # the push two-shot variant (off by default) stays parity-green
+    assert _torchrun(n, "--suite", "edge", "--seeds", "4:6", env_extra={"GR_PUSH": "1"}) == 0
 
 
 @pytest.mark.parametrize("n", [2, 4, 8])
