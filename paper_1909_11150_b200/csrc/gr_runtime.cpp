@@ -904,8 +904,9 @@ static int step_impl(gr_ctx *c, int32_t *released, gr_cycle_info *info, uint32_t
         const int ctas = drain ? c->data_ctas_full[local ? gr::ALGO_LOCAL : gr::ALGO_TWOSHOT]
                                : c->data_ctas[local ? gr::ALGO_LOCAL : gr::ALGO_TWOSHOT];
         d.lc_sub = c->lc_sub;
-        d.lag1 = c->lag1 > 0 ? c->lag1 : 2 * ctas;
-        d.lag2 = c->lag2 > 0 ? c->lag2 : 4 * ctas;
+        // queue lags (3/8 x grid measured 3-4% faster than 2/4 x grid at N=2,4)
+        d.lag1 = c->lag1 > 0 ? c->lag1 : 3 * ctas;
+        d.lag2 = c->lag2 > 0 ? c->lag2 : 8 * ctas;
         CK(c, cudaEventRecord(c->ev_bv, c->s_coord));
         CK(c, cudaStreamWaitEvent(c->s_data, c->ev_bv, 0));
         std::pair<cudaEvent_t, cudaEvent_t> evd{};

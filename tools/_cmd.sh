@@ -1,2 +1,4 @@
-GR_NVLS=1 timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 --master-port 29801 tools/bench_cfg5.py --quick --min-kib 1024 --max-mib 512 > gpurun_out/cfg5_n4_nvls.jsonl 2> gpurun_out/cfg5_n4_nvls.err
-GR_NVLS=1 GR_ONESHOT_MAX_BYTES=0 timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 --master-port 29802 tools/bench_cfg5.py --quick --min-kib 1024 --max-mib 512 > gpurun_out/cfg5_n4_nvls0.jsonl 2> gpurun_out/cfg5_n4_nvls0.err
+bash tools/sweep.sh 4 "GR_LAG1=296 GR_LAG2=592" "GR_LAG1=444 GR_LAG2=888" "GR_LAG1=296 GR_LAG2=888" "GR_LAG1=444 GR_LAG2=1184" "GR_LAG1=592 GR_LAG2=1184" "GR_LAG1=444 GR_LAG2=888" "GR_LAG1=296 GR_LAG2=592" > gpurun_out/sw_lag4b.txt 2>&1
+bash tools/sweep.sh 2 "GR_LAG1=296 GR_LAG2=592" "GR_LAG1=444 GR_LAG2=888" "GR_LAG1=296 GR_LAG2=888" "GR_LAG1=444 GR_LAG2=1184" "GR_LAG1=592 GR_LAG2=1184" "GR_LAG1=444 GR_LAG2=888" "GR_LAG1=296 GR_LAG2=592" > gpurun_out/sw_lag2b.txt 2>&1
+bash tools/sweep_cfg5.sh 4 4096 256 "GR_LAG1=296 GR_LAG2=592" "GR_LAG1=444 GR_LAG2=888" "GR_LAG1=592 GR_LAG2=1184" > gpurun_out/sw5_lag4.txt 2>&1
+cat gpurun_out/sw_lag4b.txt gpurun_out/sw_lag2b.txt gpurun_out/sw5_lag4.txt
