@@ -354,7 +354,7 @@ def main():
                 ctx.gr_mark_ready_async(t, ptrs[t], s_in.cuda_stream)
         complete, cycles = False, 0
         while not complete:
-            rel, complete, _A, _ = ctx.gr_step()
+            rel, complete, _A, _ = ctx.gr_step(bits=False)
             cycles += 1
             if rel:
                 ctx.gr_released_wait_async(s_out.cuda_stream)
@@ -470,7 +470,7 @@ def run_extras(args, ctx, grads, ptrs, tensor_order, f, N, rank, local, dev, com
         nxt = time.perf_counter()
         left, complete = f.G, False
         while left > 1:
-            rel, complete, _A, _ = ctx2.gr_step()
+            rel, complete, _A, _ = ctx2.gr_step(bits=False)
             left -= len(rel)
             if complete:
                 break

@@ -175,12 +175,13 @@ class Context:
         return _check(lib.gr_mark_ready_async(self._ctx, self.rank if rank is None else rank, tensor_id, dev_ptr,
                                               stream), self._ctx)
 
-    def gr_step(self):
-        """Returns (released group ids, step_complete, A words (list of int), info)."""
+    def gr_step(self, bits: bool = True):
+        """Returns (released group ids, step_complete, A words (list of int, or None when
+        bits=False: skips copying W words into a Python list), info)."""
         _check(lib.gr_step(self._ctx, ctypes.cast(self._released, ctypes.c_void_p), ctypes.byref(self._info),
-                           ctypes.cast(self._bits, ctypes.c_void_p)), self._ctx)
+                           ctypes.cast(self._bits, ctypes.c_void_p) if bits else None), self._ctx)
         n = self._info.n_released
-        return list(self._released[:n]), bool(self._info.step_complete), list(self._bits), self._info
+        return self._released[:n], bool(self._info.step_complete), (list(self._bits) if bits else None), self._info
 
     def gr_wait(self):
         return _check(lib.gr_wait(self._ctx), self._ctx)

@@ -140,7 +140,7 @@ class GroupedGradReducer:
         """Coordinate the step's reduction while backward is still running on the GPU
         (see drive_cycles), then order the current stream after it. Returns the cycles run."""
         def step():
-            rel, complete, _bits, _info = self.ctx.gr_step()
+            rel, complete, _bits, _info = self.ctx.gr_step(bits=False)
             return rel, complete
 
         n = drive_cycles(step, self.ctx.gr_step_drain, lambda g: self._events[g].synchronize(),

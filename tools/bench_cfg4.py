@@ -81,7 +81,7 @@ def main():
                         spin(skew)
                     s0 = ctx.stats().bitvector_device_us
                     t0 = time.perf_counter()
-                    _rel, complete, _A, _ = ctx.gr_step()
+                    _rel, complete, _A, _ = ctx.gr_step(bits=False)
                     lat.append((time.perf_counter() - t0) * 1e6)
                     kern.append(ctx.stats().bitvector_device_us - s0)
                     c += 1

@@ -80,7 +80,7 @@ def main():
 
             def ours():  # stream-ordered wait: the production contract (host never blocks on the data)
                 ctx.gr_mark_ready_prepared(batch)
-                ctx.gr_step()
+                ctx.gr_step(bits=False)
                 ctx.gr_wait_async()
 
             def ours_drain():  # every tensor marked: the device-driven cycle, no host round trip
@@ -90,7 +90,7 @@ def main():
 
             def ours_blocking():
                 ctx.gr_mark_ready_prepared(batch)
-                ctx.gr_step()
+                ctx.gr_step(bits=False)
                 ctx.gr_wait()
 
             ms = timed(ours, iters)
