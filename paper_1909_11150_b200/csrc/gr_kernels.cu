@@ -25,6 +25,7 @@
 // ld.acquire.sys on its LOCAL pad, then fence.proxy.async before the TMA reads
 // peer data. LL bitvector words carry their cycle tag in the upper 32 bits, so a
 // single 64-bit load both validates and returns the word.
+#include <atomic>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
@@ -326,13 +327,21 @@ __global__ void __launch_bounds__(NT, 1024 / NT) bitvector_kernel(BvParams p) {
     }
 }
 
+// cudaFuncSetAttribute is per device: remember, per function, the devices it was set on
+// (thread-safe; a process may drive several GPUs)
+static bool first_use_on_device(std::atomic<uint64_t> &mask) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const uint64_t bit = 1ull << (dev & 63);
+    return (mask.fetch_or(bit) & bit) == 0;
+}
+
 int launch_bitvector(const BvParams &p, void *stream) {
     const size_t smem = sizeof(uint32_t) * (3 * (size_t)p.W + ((size_t)p.G + 31) / 32);
-    static bool attr_set = false;
-    if (!attr_set) {
+    static std::atomic<uint64_t> done{0};
+    if (first_use_on_device(done)) {
         cudaFuncSetAttribute(bitvector_kernel<BV_THREADS>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
         cudaFuncSetAttribute(bitvector_kernel<1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
-        attr_set = true;
     }
     if (p.W > GR_BV_INLINE_WORDS) bitvector_kernel<1024><<<1, 1024, smem, (cudaStream_t)stream>>>(p);
     else bitvector_kernel<BV_THREADS><<<1, BV_THREADS, smem, (cudaStream_t)stream>>>(p);
@@ -1223,11 +1232,9 @@ __global__ void __maxnreg__(96) xfer_kernel(DataParams p) {
 
 template <typename BT, bool STATS>
 static int launch_data_t(const DataParams &p, int local, int ctas, cudaStream_t s) {
-    static bool attr_set = false;
-    if (!attr_set) {
+    static std::atomic<uint64_t> done{0};
+    if (first_use_on_device(done))
         cudaFuncSetAttribute(xfer_kernel<BT, STATS>, cudaFuncAttributeMaxDynamicSharedMemorySize, 208 * 1024);
-        attr_set = true;
-    }
     if (local) local_kernel<BT, STATS><<<ctas, LC_THREADS, 0, s>>>(p);
     else xfer_kernel<BT, STATS><<<ctas, XF_THREADS, (size_t)p.nstages * p.stage_bytes, s>>>(p);
     return (int)cudaGetLastError();
@@ -1272,11 +1279,8 @@ __global__ void __launch_bounds__(128) spin_kernel(int64_t ns) {
 }
 
 int launch_spin(int64_t ns, int ctas, void *stream) {
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaFuncSetAttribute(spin_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SPIN_SMEM);
-        attr_set = true;
-    }
+    static std::atomic<uint64_t> done{0};
+    if (first_use_on_device(done)) cudaFuncSetAttribute(spin_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SPIN_SMEM);
     spin_kernel<<<ctas, 128, SPIN_SMEM, (cudaStream_t)stream>>>(ns);
     return (int)cudaGetLastError();
 }
