@@ -43,6 +43,29 @@ __global__ void span_kernel(float4 *g, size_t n4) {
     }
 }
 
+// warp-contiguous spans (the local_kernel's access pattern): warp w streams SPAN float4s
+template <int U, int SPAN, bool CS>
+__global__ void warpspan_kernel(float4 *g, size_t n4) {
+    const int lane = threadIdx.x & 31;
+    const size_t gw = (size_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+    const size_t nw = (size_t)gridDim.x * (blockDim.x / 32);
+    for (size_t it = gw; it * SPAN < n4; it += nw) {
+        const size_t b = it * SPAN, e = b + SPAN < n4 ? b + SPAN : n4;
+        for (size_t i = b + lane; i < e; i += 32 * U) {
+            float4 v[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+                if (i + 32 * u < e) v[u] = CS ? __ldcs(g + i + 32 * u) : g[i + 32 * u];
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+                if (i + 32 * u < e) {
+                    if (CS) __stcs(g + i + 32 * u, rt(v[u]));
+                    else g[i + 32 * u] = rt(v[u]);
+                }
+        }
+    }
+}
+
 // TMA ring: bulk G2S tiles, convert in smem, bulk S2G back
 template <int TILE, int STAGES>
 __global__ void __launch_bounds__(256, 1) tma_kernel(float *g, size_t n) {
@@ -121,6 +144,14 @@ int main() {
         snprintf(nm, sizeof nm, "ldg U8 thr256 ctas%d", ctas);
         run(nm, [&] { ldg_kernel<8><<<ctas, 256>>>((float4 *)g, n4); });
     }
+    run("warpspan U8 span2048 thr256 ctas444", [&] { warpspan_kernel<8, 2048, false><<<444, 256>>>((float4 *)g, n4); });
+    run("warpspan U8 span2048 cs ctas444", [&] { warpspan_kernel<8, 2048, true><<<444, 256>>>((float4 *)g, n4); });
+    run("warpspan U4 span2048 ctas444", [&] { warpspan_kernel<4, 2048, false><<<444, 256>>>((float4 *)g, n4); });
+    run("warpspan U8 span8192 ctas444", [&] { warpspan_kernel<8, 8192, false><<<444, 256>>>((float4 *)g, n4); });
+    run("warpspan U8 span8192 ctas296", [&] { warpspan_kernel<8, 8192, false><<<296, 256>>>((float4 *)g, n4); });
+    run("warpspan U16 span8192 ctas296", [&] { warpspan_kernel<16, 8192, false><<<296, 256>>>((float4 *)g, n4); });
+    run("warpspan U4 span512 ctas592", [&] { warpspan_kernel<4, 512, false><<<592, 256>>>((float4 *)g, n4); });
+    run("ldg U4 thr256 ctas444", [&] { ldg_kernel<4><<<444, 256>>>((float4 *)g, n4); });
     run("ldg U4 thr512 ctas 592", [&] { ldg_kernel<4><<<592, 512>>>((float4 *)g, n4); });
     run("ldg U2 thr1024 ctas 296", [&] { ldg_kernel<2><<<296, 1024>>>((float4 *)g, n4); });
     run("span U4 thr512 ctas 296", [&] { span_kernel<4><<<296, 512>>>((float4 *)g, n4); });
