@@ -575,7 +575,7 @@ __device__ __forceinline__ int chunk_of_item(const DataParams &p, int nrel, int 
 // ---------------------------------------------------------------------------------------
 constexpr int LC_THREADS = 256;
 // warp sub-items: p.lc_sub elements each, p.lc_subs slots per chunk
-constexpr int LC_UNROLL = 4;
+constexpr int LC_UNROLL = 2;
 
 template <typename BT, bool STATS>
 __global__ void __launch_bounds__(LC_THREADS, 3) local_kernel(DataParams p) {

@@ -114,7 +114,7 @@ struct gr_ctx {
     int data_ctas_full[4] = {0, 0, 0, 0};  // every SM (drain cycles)
     int lag1 = 0, lag2 = 0;  // GR_LAG1 / GR_LAG2 overrides (tuning)
     int nstages = 4, stage_kb = 48;  // GR_STAGES / GR_STAGE_KB overrides (tuning)
-    int64_t lc_sub = 8192;           // local kernel sub-item (GR_LC_SUB, tuning)
+    int64_t lc_sub = 2048;           // local kernel sub-item (GR_LC_SUB, tuning; measured best)
     std::vector<void *> async_streams;  // distinct streams of this step's gr_mark_ready_async calls
 
     // step / cycle state
@@ -467,6 +467,8 @@ int setup_device(gr_ctx *c) {
         int rc = algo == gr::ALGO_LOCAL ? gr::data_kernel_max_ctas(algo, c->buf_f16, &mx) : 0;
         if (rc != 0) return fail(c, GR_ECUDA, "occupancy query failed: %s", cudaGetErrorString((cudaError_t)rc));
         int want = c->world.comm_ctas > 0 ? c->world.comm_ctas : mx;
+        if (algo == gr::ALGO_LOCAL)
+            if (const char *lc = getenv("GR_LOCAL_CTAS")) want = std::max(1, atoi(lc));  // tuning
         c->data_ctas[algo] = std::max(1, std::min(want, mx));
         c->data_ctas_full[algo] = std::max(1, mx);
     }

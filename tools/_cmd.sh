@@ -1,3 +1,3 @@
-timeout 300 python -c "import __graft_entry__ as g; g.build(); g.smoke(); print('smoke ok')" > gpurun_out/smoke.log 2>&1; tail -2 gpurun_out/smoke.log
-timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/ref.json 2> gpurun_out/ref.err; tail -1 gpurun_out/ref.json | cut -c1-400
-timeout 600 python bench.py > gpurun_out/bench_n1.json 2> gpurun_out/bench_n1.err; tail -1 gpurun_out/bench_n1.json | cut -c1-300
+bash tools/sweep1.sh "GR_LC_SUB=2048" "GR_LC_SUB=1024" > gpurun_out/sw1_u2c.txt 2>&1; cat gpurun_out/sw1_u2c.txt
+cp paper_1909_11150_b200/libgr.so /tmp/libgr_u2.so; cp gpurun_out/var/libgr_u1.so paper_1909_11150_b200/libgr.so
+bash tools/sweep1.sh "GR_LC_SUB=2048" "GR_LC_SUB=4096" "GR_LC_SUB=1024" > gpurun_out/sw1_u1.txt 2>&1; cat gpurun_out/sw1_u1.txt
