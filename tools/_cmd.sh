@@ -1,3 +1,3 @@
-bash tools/sweep1.sh "GR_LC_SUB=2048" "GR_LC_SUB=1024" > gpurun_out/sw1_u2c.txt 2>&1; cat gpurun_out/sw1_u2c.txt
-cp paper_1909_11150_b200/libgr.so /tmp/libgr_u2.so; cp gpurun_out/var/libgr_u1.so paper_1909_11150_b200/libgr.so
-bash tools/sweep1.sh "GR_LC_SUB=2048" "GR_LC_SUB=4096" "GR_LC_SUB=1024" > gpurun_out/sw1_u1.txt 2>&1; cat gpurun_out/sw1_u1.txt
+timeout 300 python bench.py --steps 3 --warmup 3 --no-extras > gpurun_out/plain2.json 2>&1 && \
+timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"local_kernel|bitvector" -s 4 -c 4 -o gpurun_out/r01c_n1_full python bench.py --steps 3 --warmup 3 --no-extras > gpurun_out/ncu_f.log 2>&1
+echo rc=$?
