@@ -102,7 +102,19 @@ __global__ void __launch_bounds__(NT, 1024 / NT) bitvector_kernel(BvParams p) {
     // ready = host marks (gr_mark_ready, bits) | async marks (device flag == epoch, ballot);
     // pending = ready & ~released (reading R4: a ready tensor stays pending until its group goes)
     uint64_t *my_slot = p.slot[p.rank] + (size_t)p.parity * W;
-    for (int w0 = warp; w0 < W; w0 += nwarps * BV_BATCH) {
+    if (!p.check_async) {  // host marks only: a thread per word, no per-bit flags to gather
+        for (int w = tid; w < W; w += blockDim.x) {
+            const uint32_t hbw = p.use_inline ? p.inline_bits[w] : p.host_bits[w];
+            const int lo = (w == 0) ? GR_STATUS_BITS : 0;
+            const int hi = min(32, p.nbits - w * 32);
+            const uint32_t valid = (hi >= 32 ? 0xffffffffu : ((1u << hi) - 1u)) & ~((1u << lo) - 1u);
+            uint32_t word = hbw & valid & ~sR[w];
+            if (w == 0) word |= (p.abort_flag ? 0u : 1u) | (p.shutdown_flag ? 0u : 2u);  // complement-coded (R1)
+            sL[w] = word;
+            st_relaxed_sys64(my_slot + w, ((uint64_t)p.tag << 32) | word);
+        }
+    }
+    for (int w0 = warp; p.check_async && w0 < W; w0 += nwarps * BV_BATCH) {
         uint32_t f[BV_BATCH], hb[BV_BATCH];
 #pragma unroll
         for (int k = 0; k < BV_BATCH; ++k) {  // issue the independent loads first

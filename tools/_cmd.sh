@@ -1,3 +1,3 @@
-timeout 300 python bench.py --steps 3 --warmup 3 --no-extras > gpurun_out/plain2.json 2>&1 && \
-timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"local_kernel|bitvector" -s 4 -c 4 -o gpurun_out/r01c_n1_full python bench.py --steps 3 --warmup 3 --no-extras > gpurun_out/ncu_f.log 2>&1
-echo rc=$?
+timeout 1200 python -m pytest tests/test_gpu_parity.py -q -x -k "n1 or errors or async or drain or multi_gpu_cfg1 or multi_gpu_edge" > gpurun_out/pt_bv.log 2>&1; tail -2 gpurun_out/pt_bv.log
+timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 --master-port 29901 tools/bench_cfg4.py --cycles 1000 --skew-us 0,10 --no-baselines > gpurun_out/cfg4_d.jsonl 2> gpurun_out/cfg4_d.err
+grep '^{' gpurun_out/cfg4_d.jsonl

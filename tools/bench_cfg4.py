@@ -32,6 +32,8 @@ def main():
     ap.add_argument("--cycles", type=int, default=2000)
     ap.add_argument("--skew-us", default="0,10,100")
     ap.add_argument("--tmax", type=int, default=65536)
+    ap.add_argument("--tmin", type=int, default=64)
+    ap.add_argument("--no-baselines", action="store_true")
     a = ap.parse_args()
 
     import numpy as np
@@ -57,7 +59,7 @@ def main():
         while time.perf_counter() < t:
             pass
 
-    T = 64
+    T = a.tmin
     while T <= a.tmax:
         case = cfg4_case(T, N)
         grads = torch.zeros(T * 8, device=dev)
@@ -104,6 +106,9 @@ def main():
                        "kernel_us_p99": round(max(r["kernel_us_p99"] for r in allres), 2)}
                 print(json.dumps(out), flush=True)
         ctx.gr_finalize()
+        if a.no_baselines:
+            T *= 4
+            continue
         # baselines on the same box
         flags = torch.ones(T, dtype=torch.uint8, device=dev)
         for _ in range(20):
