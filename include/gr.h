@@ -75,7 +75,7 @@ typedef struct {
     int32_t timeout_ms;         /* bound on any cross-rank wait; 0 = 20000 */
     int32_t comm_ctas;          /* CTAs of the fused reduce kernel; 0 = library default */
     int64_t chunk_elems;        /* fusion-buffer chunk (pipelining) granularity in elements,
-                                   multiple of 8; 0 = adaptive per group (about two chunks per
+                                   multiple of 8; 0 = adaptive per group (about one chunk per
                                    SM, a power of two between 8K and 128K elements) */
     gr_allgather_fn allgather;  /* required when world_size > 1 */
     void *user;                 /* passed to allgather */

@@ -58,7 +58,7 @@ struct gr_ctx {
     bool dry = false;
     int buf_f16 = 1;
     int64_t chunk_elems = 0;  // 0 = adaptive per group
-    int64_t chunk_target_div = 296, chunk_max = 131072;  // adaptive rule (GR_CHUNK_DIV / GR_CHUNK_MAX)
+    int64_t chunk_target_div = 148, chunk_max = 131072;  // adaptive rule (GR_CHUNK_DIV / GR_CHUNK_MAX)
     int64_t one_shot_max_bytes = 0;
     uint64_t hash = 0;
 
@@ -282,7 +282,7 @@ int build_layouts(gr_ctx *c, const gr_tensor *table, const int32_t *group_of) {
         c->gchunk_begin[g] = (int32_t)c->chunks.size();
         const int32_t pos0 = pos;
         while (pos < T && group_of[order[pos]] == g) ++pos;
-        // chunk size: fixed when the caller asks for one; otherwise per group, about two chunks
+        // chunk size: fixed when the caller asks for one; otherwise per group, about one chunk
         // per SM for the group alone (power of two in [8K, 128K] elements): large groups get
         // large items (fewer flags, longer TMA streams), small ones keep every SM busy
         int64_t cg = c->chunk_elems;
