@@ -1,4 +1,9 @@
-timeout 1500 python -m pytest tests -m gpu -q -x > gpurun_out/pt_final.log 2>&1; tail -3 gpurun_out/pt_final.log
-timeout 600 python bench.py > gpurun_out/bench_n1.json 2> gpurun_out/bench_n1.err
-timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29668 bench.py --gpus 2 > gpurun_out/bench_n2.json 2> gpurun_out/bench_n2.err
-timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 --master-port 29667 bench.py --gpus 4 > gpurun_out/bench_n4.json 2> gpurun_out/bench_n4.err
+GR_TRACE=gpurun_out/trf GR_TRACE_MAX_CYCLES=6 timeout 300 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 --master-port 29911 bench.py --gpus 4 --steps 3 --warmup 3 --no-extras > gpurun_out/trf.log 2>&1
+python tools/trace_summary.py gpurun_out/trf > gpurun_out/trf_sum.txt 2>&1; rm -f gpurun_out/trf.rank*.jsonl
+for n in 2 4; do
+R="python -m torch.distributed.run --nnodes=1 --nproc-per-node $n --master-addr 127.0.0.1 --master-port 29777 tools/bench_train.py --batch 8"
+timeout 300 $R --impl ours >> gpurun_out/trf_train.jsonl 2>>gpurun_out/trf_train.err
+timeout 300 $R --impl ours --drain-tail 8 >> gpurun_out/trf_train.jsonl 2>>gpurun_out/trf_train.err
+timeout 300 $R --impl ddp >> gpurun_out/trf_train.jsonl 2>>gpurun_out/trf_train.err
+done
+timeout 300 python tools/bench_train.py --impl none --batch 8 >> gpurun_out/trf_train.jsonl 2>>gpurun_out/trf_train.err
