@@ -660,8 +660,10 @@ __global__ void __launch_bounds__(LC_THREADS, 3) local_kernel(DataParams p) {
 //     flags, and streams the peers' fusion-buffer sub-tiles into a ring of shared-memory
 //     stages with cp.async.bulk (TMA bulk copies from NVLink peer memory, mbarrier
 //     complete_tx) — the remote latency is hidden by the ring, not by registers;
-//   warps 1..15 = consumers: pack (local LDG/STG), reduce in rank order from the staged
-//     copies + own gradients, scale, round, unpack; push chunk flags to peers.
+//   warp 1 / lane 0 = publisher: takes finished chunks from the consumers (mbarrier ring),
+//     fence.sc.sys, then pushes the chunk flags to the peers (the fence is off the data path);
+//   warps 2..15 = consumers: pack (TMA-staged gradients -> buffer), reduce in rank order from
+//     the staged copies + own gradients, scale, round, unpack (NVLS: multimem reductions).
 // Work queue: triples k = 0,1,.. each holding {PACK(k), RED/RS(k-L1), AG(k-L2)} of the
 // released chunk list; every rank takes them in the same order, so every dependency
 // (PACK(j) before RED/RS(j) before AG(j)) points backwards in every queue: no deadlock,
