@@ -1,9 +1,7 @@
-GR_TRACE=gpurun_out/trf GR_TRACE_MAX_CYCLES=6 timeout 300 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 --master-port 29911 bench.py --gpus 4 --steps 3 --warmup 3 --no-extras > gpurun_out/trf.log 2>&1
-python tools/trace_summary.py gpurun_out/trf > gpurun_out/trf_sum.txt 2>&1; rm -f gpurun_out/trf.rank*.jsonl
 for n in 2 4; do
-R="python -m torch.distributed.run --nnodes=1 --nproc-per-node $n --master-addr 127.0.0.1 --master-port 29777 tools/bench_train.py --batch 8"
-timeout 300 $R --impl ours >> gpurun_out/trf_train.jsonl 2>>gpurun_out/trf_train.err
-timeout 300 $R --impl ours --drain-tail 8 >> gpurun_out/trf_train.jsonl 2>>gpurun_out/trf_train.err
-timeout 300 $R --impl ddp >> gpurun_out/trf_train.jsonl 2>>gpurun_out/trf_train.err
-done
-timeout 300 python tools/bench_train.py --impl none --batch 8 >> gpurun_out/trf_train.jsonl 2>>gpurun_out/trf_train.err
+for suite in "edge --seeds 0:4" "cfg1 --seeds 0:10" "stats --seeds 0:2" "fcn --seeds 5:6 --buffers f16" "drain --seeds 0:4"; do
+GR_RS_SPLIT=1 timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node $n --master-addr 127.0.0.1 --master-port 29555 tests/mp_worker.py --suite $suite > gpurun_out/split_$n.log 2>&1; echo "N=$n $suite rc=$?"; grep "mp_worker suite" gpurun_out/split_$n.log
+done; done
+bash tools/sweep.sh 4 "GR_RS_SPLIT=0" "GR_RS_SPLIT=1" "GR_RS_SPLIT=0" "GR_RS_SPLIT=1" > gpurun_out/sw_split4.txt 2>&1; cat gpurun_out/sw_split4.txt
+bash tools/sweep.sh 2 "GR_RS_SPLIT=0" "GR_RS_SPLIT=1" > gpurun_out/sw_split2.txt 2>&1; cat gpurun_out/sw_split2.txt
+bash tools/sweep_cfg5.sh 4 4096 256 "GR_RS_SPLIT=0" "GR_RS_SPLIT=1" > gpurun_out/sw5_split4.txt 2>&1; cat gpurun_out/sw5_split4.txt
