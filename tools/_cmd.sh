@@ -1,5 +1,6 @@
-for n in 2 4; do
-for suite in "edge --seeds 0:3" "fcn --seeds 7:8 --buffers f16" "stats --seeds 0:2"; do
-GR_NVLS=1 timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node $n --master-addr 127.0.0.1 --master-port 29555 tests/mp_worker.py --suite $suite > gpurun_out/nsplit_$n.log 2>&1; echo "N=$n $suite rc=$?"; grep "mp_worker suite" gpurun_out/nsplit_$n.log
-done; done
-bash tools/sweep.sh 4 "GR_NVLS=1 GR_NRS_SPLIT=0" "GR_NVLS=1 GR_NRS_SPLIT=1" "GR_NVLS=1 GR_NRS_SPLIT=0" "GR_NVLS=1 GR_NRS_SPLIT=1" > gpurun_out/sw_nsplit4.txt 2>&1; cat gpurun_out/sw_nsplit4.txt
+timeout 1500 python -m pytest tests -m gpu -q -x > gpurun_out/pt_final2.log 2>&1; tail -3 gpurun_out/pt_final2.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" 2>&1 | tail -1
+timeout 600 python bench.py > gpurun_out/final_n1.json 2> gpurun_out/final_n1.err
+timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29668 bench.py --gpus 2 > gpurun_out/final_n2.json 2> gpurun_out/final_n2.err
+timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 --master-port 29667 bench.py --gpus 4 > gpurun_out/final_n4.json 2> gpurun_out/final_n4.err
+timeout 300 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 --master-port 29669 bench.py --impl reference --gpus 4 --steps 2 --warmup 1 > gpurun_out/final_ref4.json 2> gpurun_out/final_ref4.err
