@@ -145,3 +145,20 @@ def test_gloo_world2_init_consistency(mismatch):
     else:
         assert all(r[1] == "ok" for r in res), res
         assert res[0][2:] == res[1][2:]
+
+
+def test_plain_c_program_uses_the_abi(tmp_path):
+    """The boundary is a C ABI: a C11 program compiled against include/gr.h alone and linked
+    with libgr.so (no Python, no torch in that process) builds a dry context and checks the
+    response cache against reading R3, the fusion layout and the error paths."""
+    import shutil
+    import subprocess
+    if shutil.which("gcc") is None:
+        pytest.skip("gcc not available")
+    pkg = os.path.join(ROOT, "paper_1909_11150_b200")
+    exe = str(tmp_path / "abi_dry")
+    subprocess.run(["gcc", "-std=c11", "-Wall", "-Wextra", "-Werror", "-I", os.path.join(ROOT, "include"),
+                    os.path.join(ROOT, "tests", "c", "abi_dry.c"), "-L", pkg, "-lgr", f"-Wl,-rpath,{pkg}",
+                    "-o", exe], check=True)
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=60)
+    assert r.returncode == 0 and r.stdout.strip() == "ok", (r.stdout, r.stderr)
