@@ -48,6 +48,8 @@ def parse():
     ap.add_argument("--cycle-us", type=float, default=250.0)
     ap.add_argument("--comm-sms", type=int, default=16)
     ap.add_argument("--no-extras", action="store_true", help="skip exposed-comm / cycle / NCCL / CPU legs")
+    ap.add_argument("--exposed-sweep", default="",
+                    help="cfg3 sweep only: 'cycle_us:comm_sms,...' pairs, one JSON line each, then exit")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     return ap.parse_args()
 
@@ -175,6 +177,14 @@ def run_reference(args):
     print(json.dumps(out), flush=True)
 
 
+def _max_over(x: float, dev) -> float:
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
 # ------------------------------------------------------------------ our arm
 def main():
     args = parse()
@@ -224,6 +234,16 @@ def main():
     def barrier():
         if N > 1:
             dist.barrier(device_ids=[local])
+
+    if args.exposed_sweep:  # cfg3 sweep of the cycle time and of the SMs given to communication
+        for pair in args.exposed_sweep.split(","):
+            cu, cs = pair.split(":")
+            r = exposed_comm(args, float(cu), int(cs), f, ptrs, N, rank, local, dev, compute, sms, barrier,
+                             lambda x: x if N == 1 else _max_over(x, dev), gr)
+            if rank == 0:
+                print(json.dumps({"cfg3_sweep": True, "n_gpus": N, **r["exposed_comm"]}), flush=True)
+        ctx.gr_finalize()
+        return
 
     batch = ctx.prepare_batch(tensor_order, [ptrs[t] for t in tensor_order])
 
@@ -437,22 +457,21 @@ def main():
         dist.destroy_process_group()
 
 
-def run_extras(args, ctx, grads, ptrs, tensor_order, f, N, rank, local, dev, compute, sms, barrier,
-               max_over_ranks, gr):
-    """cfg3 exposed comm (synthetic backward), cycle latency, NCCL baseline."""
+def exposed_comm(args, cycle_us, comm_sms, f, ptrs, N, rank, local, dev, compute, sms, barrier, max_over_ranks, gr):
+    """cfg3: exposed communication behind a synthetic backward pass. Reported
+    two ways: per rank (own end of comm - own end of backward, then max / mean over ranks; it
+    includes waiting for a slower rank), and SURVEY's definition max_r end of comm - max_r end of
+    backward (the start events follow a barrier + device sync on every rank)."""
     import numpy as np
     import torch
     import torch.distributed as dist
 
-    out = {}
-    # ---- exposed communication with a synthetic backward (SURVEY.md §8(d) cfg3) ----
-    comm_sms = args.comm_sms
     ctx2 = gr.Context(rank=rank, world_size=N, device=local, numel=f.numel, group_of=f.group_of,
                       buffer_dtype=gr.GR_F16 if args.buffer == "f16" else gr.GR_F32,
                       compute_stream=compute.cuda_stream, timeout_ms=30000, comm_ctas=comm_sms,
                       allgather=gr.make_allgather(None, local) if N > 1 else None)
-    cyc = args.cycle_us * 1e-6
-    exposed, bwd = [], []
+    cyc = cycle_us * 1e-6
+    exposed, bwd, survey = [], [], []
     for step in range(args.exposed_steps + 2):
         rng = np.random.default_rng(1000003 * step + rank)
         barrier()
@@ -488,6 +507,7 @@ def run_extras(args, ctx, grads, ptrs, tensor_order, f, N, rank, local, dev, com
         if step >= 2:
             exposed.append(max(0.0, ev_bwd.elapsed_time(ev_end)))
             bwd.append(ev_start.elapsed_time(ev_bwd))
+            survey.append(max_over_ranks(ev_start.elapsed_time(ev_end)) - max_over_ranks(bwd[-1]))
     ex_max = [max_over_ranks(x) for x in exposed]
     ex_mean_local = float(np.mean(exposed))
     ex_mean = ex_mean_local
@@ -495,16 +515,31 @@ def run_extras(args, ctx, grads, ptrs, tensor_order, f, N, rank, local, dev, com
         tt = torch.tensor([ex_mean_local], dtype=torch.float64, device=dev)
         dist.all_reduce(tt)
         ex_mean = float(tt.item()) / N
+    out = {}
     out["exposed_comm_ms"] = round(float(np.mean(ex_max)), 4)
     out["exposed_comm"] = {"ms_per_step_max_over_ranks": round(float(np.mean(ex_max)), 4),
                            "ms_per_step_mean_over_ranks": round(ex_mean, 4),
+                           "ms_per_step_survey_def": round(max(0.0, float(np.mean(survey))), 4),
                            "t_bwd_ms": round(float(np.mean(bwd)), 3),
                            "frac_of_bwd": round(float(np.mean(ex_max)) / float(np.mean(bwd)), 5),
-                           "cycle_us": args.cycle_us, "comm_sms": comm_sms, "steps": len(exposed),
+                           "cycle_us": cycle_us, "comm_sms": comm_sms, "steps": len(exposed),
                            "compute": "gr_bench_spin per layer, d_l=2*OPS_l/(0.70*1401.8 TF/s) x U(0.9,1.1)",
                            "marks": "gr_mark_ready_async on the compute stream after each layer",
-                           "cycles": "host tics while backward runs; the last group by gr_step_drain"}
+                           "cycles": "host tics while backward runs; the last group by gr_step_drain",
+                           "survey_def": "max_r end of comm - max_r end of backward (SURVEY.md §8(d) cfg3)"}
     ctx2.gr_finalize()
+    return out
+
+
+def run_extras(args, ctx, grads, ptrs, tensor_order, f, N, rank, local, dev, compute, sms, barrier,
+               max_over_ranks, gr):
+    """cfg3 exposed comm (synthetic backward), cycle latency, NCCL baseline."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    out = exposed_comm(args, args.cycle_us, args.comm_sms, f, ptrs, N, rank, local, dev, compute, sms,
+                       barrier, max_over_ranks, gr)
 
     # ---- NEXT-2 epilogue cost: the same step with the fused ||g||^2 / non-finite statistics ----
     batch = ctx.prepare_batch(tensor_order, [ptrs[t] for t in tensor_order])
