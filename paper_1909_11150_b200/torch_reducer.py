@@ -4,9 +4,11 @@ autograd backward pass.
 `GroupedGradReducer` registers a post-accumulate-grad hook on every parameter; the hook marks
 the gradient ready with `gr_mark_ready_async` on the stream autograd is using, so the ready
 flag is written by the GPU right after the gradient exists ("pending requests").
-`synchronize()` then runs coordination cycles ("tics") until every group has been
-released — complete groups are reduced while the GPU is still running the rest of the backward
-pass — and makes the current stream wait for the reduced gradients (no host block).
+`synchronize()` then runs coordination cycles ("tics") as groups become ready —
+complete groups are reduced while the GPU is still running the rest of the backward pass — ends
+the step with one device-driven drain cycle (`gr_step_drain`), and makes the current stream
+wait for the reduced gradients (no host block). One backward pass per `synchronize()`; every
+parameter must receive a gradient (a hook that never fires leaves its group unreleased).
 
 Argument marshalling only: all arithmetic runs in libgr.so. Groups default to the paper's
 usage — a few contiguous groups of roughly equal bytes in reverse registration order (the
@@ -96,8 +98,10 @@ class GroupedGradReducer:
     """comm_ctas bounds the SMs a reduction occupies while backward is still running (0 = every
     SM; the fused kernel holds a large shared-memory ring, so each of its CTAs displaces compute
     on its SM); the step's final, device-driven cycle (gr_step_drain) always uses every SM.
-    Defaults are the best measured on a 51M-parameter FC-DenseNet at N=2/4 (tools/bench_train.py,
-    DESIGN.md §11): 4 groups, full grid, drain of the last group."""
+    Defaults (4 groups, full grid, per-group cycles, drain of the last group) are the best
+    overlapped setting measured on a 51M-parameter FC-DenseNet at N=2/4 (tools/bench_train.py,
+    profiles/r01_train/); at that scale one drain cycle after backward
+    (`synchronize(drain_tail=n_groups)`) is ~1% faster still."""
 
     def __init__(self, params, *, rank: int, world_size: int, device: int, groups=None, n_groups: int = 4,
                  buffer_dtype: int = GR_F16, pg=None, timeout_ms: int = 0, comm_ctas: int = 0):
