@@ -1,2 +1,6 @@
-timeout 600 python bench.py > gpurun_out/v_n1.json 2> gpurun_out/v_n1.err; tail -1 gpurun_out/v_n1.json | cut -c1-200
-timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29668 bench.py --gpus 2 > gpurun_out/v_n2.json 2> gpurun_out/v_n2.err; tail -1 gpurun_out/v_n2.json | cut -c1-200
+timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 --master-port 29801 tools/bench_cfg5.py --tensors 16 --min-kib 64 --max-mib 1024 --iters 10 > gpurun_out/cfg5_n4_t16.jsonl 2> gpurun_out/cfg5_n4_t16.err
+grep bytes gpurun_out/cfg5_n4_t16.jsonl | python -c "
+import json,sys
+for l in sys.stdin:
+    d=json.loads(l); print(d['bytes'], d['tensors'], round(d['default_us'],1), round(d['default_drain_us'],1), round(d['nccl_us'],1), round(d['default_drain_busbw'],1), round(d['nccl_busbw'],1))
+"

@@ -25,6 +25,8 @@ def main():
     ap.add_argument("--max-mib", type=int, default=1024)
     ap.add_argument("--iters", type=int, default=20)
     ap.add_argument("--quick", action="store_true", help="library default only, no NCCL (tuning sweeps)")
+    ap.add_argument("--tensors", type=int, default=1, help="split the message into this many tensors "
+                    "(separate allocations) of one group (SURVEY.md cfg5's 16-tensor variant)")
     a = ap.parse_args()
 
     import torch
@@ -69,14 +71,16 @@ def main():
     for S in sizes:
         n = S // pb
         iters = a.iters if S <= (64 << 20) else max(5, a.iters // 4)
-        g = torch.randn(n, device=dev)
-        res = {"bytes": S, "elems": n}
+        k = max(1, min(a.tensors, n // 8))
+        sizes_t = [n // k + (1 if i < n % k else 0) for i in range(k)]
+        gs = [torch.randn(m, device=dev) for m in sizes_t]
+        res = {"bytes": S, "elems": n, "tensors": k}
         variants = (("default", -1),) if a.quick else (("default", -1), ("oneshot", 1 << 62), ("twoshot", 0))
         for name, osm in variants:
-            ctx = gr.Context(rank=rank, world_size=N, device=local, numel=[n], group_of=[0],
+            ctx = gr.Context(rank=rank, world_size=N, device=local, numel=sizes_t, group_of=[0] * k,
                              buffer_dtype=gr.GR_F16 if pb == 2 else gr.GR_F32, compute_stream=comp.cuda_stream,
                              one_shot_max_bytes=osm, timeout_ms=30000, allgather=ag)
-            batch = ctx.prepare_batch([0], [g.data_ptr()])
+            batch = ctx.prepare_batch(list(range(k)), [x.data_ptr() for x in gs])
 
             def ours():  # stream-ordered wait: the production contract (host never blocks on the data)
                 ctx.gr_mark_ready_prepared(batch)
