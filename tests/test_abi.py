@@ -162,3 +162,40 @@ def test_plain_c_program_uses_the_abi(tmp_path):
                     "-o", exe], check=True)
     r = subprocess.run([exe], capture_output=True, text=True, timeout=60)
     assert r.returncode == 0 and r.stdout.strip() == "ok", (r.stdout, r.stderr)
+
+
+def _cuobjdump(*args):
+    import shutil
+    import subprocess
+    exe = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
+    if not os.path.exists(exe):
+        pytest.skip("cuobjdump not installed")
+    from paper_1909_11150_b200 import binding
+    return subprocess.run([exe, *args, binding.LIB_PATH], capture_output=True, text=True).stdout
+
+
+def test_kernel_resource_budgets():
+    """The register / local-memory budgets the design relies on: no kernel
+    spills to local memory; the N=1 kernel fits 4 CTAs x 256 threads per SM (<= 64 registers);
+    the fused reduce kernel stays at <= 96 x 512 and the bitvector kernel at <= 64 x 256, so the
+    next cycle's bitvector kernel can be resident beside a running reduction."""
+    out = _cuobjdump("--dump-resource-usage")
+    rows = re.findall(r"Function (\S+):\s*\n\s*REG:(\d+) STACK:(\d+) SHARED:(\d+) LOCAL:(\d+)", out)
+    assert len(rows) >= 10, out[:2000]
+    for name, reg, _stack, _shared, local in rows:
+        reg, local = int(reg), int(local)
+        assert local == 0, f"{name} uses {local} B of local memory"
+        if "local_kernel" in name and "Lb0E" in name:
+            assert reg <= 64, f"{name}: {reg} registers"
+        if "xfer_kernel" in name:
+            assert reg <= 96, f"{name}: {reg} registers"
+        if "bitvector_kernel" in name:
+            assert reg <= 64, f"{name}: {reg} registers"
+
+
+def test_fused_reduce_kernel_uses_tma_and_multimem():
+    """SASS evidence (B200_PROFILING.md mnemonics): the fused reduce kernel stages peer data with
+    TMA bulk copies (UBLKCP) completed on mbarriers (SYNCS.*TRANS64) and carries the NVLS
+    in-switch reduction (LDGMC = multimem.ld_reduce)."""
+    sass = _cuobjdump("-sass", "-fun", "_ZN2gr11xfer_kernelI6__halfLb0EEEvNS_10DataParamsE")
+    assert "UBLKCP" in sass and "SYNCS.ARRIVE.TRANS64" in sass and "LDGMC" in sass
