@@ -435,7 +435,8 @@ def main():
     if rank == 0:
         out = {"metric": METRIC, "value": round(value, 3), "unit": "GB/s", "n_gpus": N, "steps": args.steps,
                "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "weak",
-               "vs_baseline": None, "dtype": "f32-grad/f16-wire" if buf16 else "f32",
+               "vs_baseline": None, "dtype": "f32", "wire_dtype": "f16" if buf16 else "f32",
+               "dtype_note": "fp32 gradients, fp32 accumulation; the fusion buffer / NVLink wire holds fp16 (RN-even) with --buffer f16",
                "data": "synthetic (counter-based seeded fp32 gradients; fcn220m shapes, SURVEY.md App. A)",
                "config": {"workload": "fcn220m_cfg2_pack_scale_unpack" if N == 1 else "fcn220m_cfg3_bitvector_grouping",
                           "tensors": f.T, "groups": f.G, "elements": E, "buffer": args.buffer,
