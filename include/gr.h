@@ -182,7 +182,8 @@ int gr_wait_async(gr_ctx *ctx);
  * the next gr_wait / gr_wait_async / gr_step. */
 int gr_step_drain(gr_ctx *ctx);
 
-/* gr_released_wait_async — LOCAL. Makes `stream` (a cudaStream_t; NULL = world.compute_stream)
+/* gr_released_wait_async — LOCAL. Makes `stream` (a cudaStream_t, borrowed; NULL =
+ * world.compute_stream)
  * wait for the reduction of every group released so far in this step, without ending the step
  * or blocking the host: work enqueued on `stream` afterwards sees those groups' reduced
  * gradients (e.g. a device->host copy or an optimizer update of the layers whose gradients are
