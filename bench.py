@@ -28,7 +28,6 @@ import os
 import statistics
 import subprocess
 import sys
-import threading
 import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
@@ -116,7 +115,6 @@ def cpu_oracle_leg(N: int, seconds: float, buffer_f16: bool):
 
     import oracle
     from workloads import fcn220m
-    from workloads.schedules import reverse_layer_schedule
     from workloads.values import tensor_scales, values_np
 
     f = fcn220m()

@@ -94,7 +94,6 @@ def main():
     import torch.distributed as dist
 
     from paper_1909_11150_b200 import GR_F16, GR_F32, Context, make_allgather
-    from paper_1909_11150_b200.binding import GR_Q_NVLS
     from tests.parity_lib import check_grad_stats, run_case_on_rank
     from workloads import cfg1_case, fcn220m
     from workloads.schedules import Case, random_mark_schedule, random_partition, reverse_layer_schedule

@@ -1,5 +1,5 @@
 """Probe the GPU box: topology, P2P, multicast, host cores. Writes gpurun_out/probe.txt."""
-import ctypes, os, subprocess, sys
+import ctypes, os, subprocess
 out = []
 def p(*a):
     s = " ".join(str(x) for x in a); print(s); out.append(s)
