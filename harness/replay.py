@@ -18,9 +18,11 @@ class ReplayLog:
 
 
 def replay_step(ctx, mark_cycle, ptrs, max_cycles: int = 1000, async_stream=None,
-                drain_after: int = -1) -> ReplayLog:
+                drain_after: int = -1, before_step=None) -> ReplayLog:
     """drain_after >= 0: after that many gr_step cycles (unless the step completed), mark every
-    remaining tensor in schedule order and end the step with one gr_step_drain."""
+    remaining tensor in schedule order and end the step with one gr_step_drain.
+    before_step(): called before every gr_step (e.g. to let stream-ordered marks land, so the
+    cycle sees exactly the schedule's marks, as the oracle assumes)."""
     by_cycle: dict[int, list[int]] = {}
     for t, m in enumerate(mark_cycle):
         if m >= 0:
@@ -44,6 +46,8 @@ def replay_step(ctx, mark_cycle, ptrs, max_cycles: int = 1000, async_stream=None
                 ctx.gr_mark_ready(t, ptrs[t])
             else:
                 ctx.gr_mark_ready_async(t, ptrs[t], async_stream)
+        if before_step is not None:
+            before_step()
         rel, complete, A, _info = ctx.gr_step()
         log.A.append(A)
         log.released.append(rel)

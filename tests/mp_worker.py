@@ -177,6 +177,15 @@ def main():
                     gf = (rng.random(T) < 0.3).tolist()
                     for osm in (0, 1 << 62):
                         run(case, seed, buf, grad_f16=gf, osm=osm, stats=True)
+            elif args.suite == "bigT":  # bitvectors beyond the inline size, up to T = 65,536
+                from workloads import cfg4_case
+                for seed in range(s0, s1):
+                    for T, rand_groups in ((4096, True), (65536, False)):
+                        base = cfg4_case(T, N, marks_per_cycle=T // 5)
+                        rng = np.random.default_rng(T + seed)
+                        group_of = random_partition(T, T // 8, rng) if rand_groups else base.group_of
+                        numel = rng.integers(1, 64, size=T).astype(np.int64)
+                        run(Case(N, numel, group_of, base.mark_cycle, seed), seed, buf)
             elif args.suite == "drain":
                 from tests.parity_lib import run_drain_case_on_rank
                 stream = torch.cuda.Stream(device=dev)

@@ -76,7 +76,7 @@ def check_values(out_np, gs, N, buffer_f16: bool, grad_f16_t: bool, where="", ex
 
 
 def run_case_on_rank(ctx, case, r, seed, device, buffer_f16: bool, grad_f16=None, kind="uniform",
-                     max_cycles=None, async_stream=None, exact: bool = True):
+                     max_cycles=None, async_stream=None, exact: bool = True, before_step=None):
     """Replay `case` on rank r through the C ABI and check it against the oracle.
     Returns (log, sha256 of all output gradients) for the cross-rank comparison."""
     import torch
@@ -87,7 +87,7 @@ def run_case_on_rank(ctx, case, r, seed, device, buffer_f16: bool, grad_f16=None
     grads = make_grads(case.numel, r, seed, device, grad_f16, kind)
     torch.cuda.synchronize(device)
     log = replay_step(ctx, case.mark_cycle[r], [g.data_ptr() for g in grads], max_cycles,
-                      async_stream=async_stream)
+                      async_stream=async_stream, before_step=before_step)
     ref = oracle.simulate_step(case.N, case.group_of, case.mark_cycle, max_cycles=max_cycles)
     check_schedule(log, ref, where=f"rank {r} seed {seed}")
     released_groups = {g for rel in ref.released for g in rel}

@@ -266,6 +266,30 @@ def test_step_drain_requires_every_mark(gpu):
     ctx.gr_finalize()
 
 
+@pytest.mark.parametrize("T,rand_groups", [(4096, True), (65536, False)])
+def test_large_tables_n1(gpu, T, rand_groups):
+    """Bitvectors beyond the inline-parameter size (W > 64 words: mark bits DMA'd, 1024-thread
+    bitvector kernel, thread-per-word populate) up to cfg4's largest table (T = 65,536, W = 2,049):
+    schedule and A words bit-exact, values bit-exact; host marks and stream-ordered marks (the
+    warp-ballot populate over 65,536 per-tensor flags)."""
+    import torch
+    from tests.parity_lib import run_case_on_rank
+    from workloads import cfg4_case
+    base = cfg4_case(T, 1, marks_per_cycle=T // 5)
+    rng = np.random.default_rng(T)
+    group_of = random_partition(T, T // 8, rng) if rand_groups else base.group_of
+    numel = rng.integers(1, 64, size=T).astype(np.int64)
+    case = Case(1, numel, group_of, base.mark_cycle, 17)
+    for buf16, async_marks in ((True, False), (False, True)):
+        ctx = _ctx(case, buf16)
+        s = torch.cuda.Stream(device=gpu) if async_marks else None
+        # stream-ordered marks become visible when their stream runs the write; letting the
+        # stream drain before each cycle makes the cycle see exactly the schedule's marks
+        run_case_on_rank(ctx, case, 0, 17, gpu, buf16, async_stream=s.cuda_stream if s else None,
+                         before_step=s.synchronize if s else None)
+        ctx.gr_finalize()
+
+
 def test_fcn220m_n1_full_size(gpu):
     """The bench workload at full size (225,115,137 elements, 68 tensors,
     10 groups), reverse-layer schedule; values checked on sampled elements."""
@@ -343,6 +367,15 @@ def test_multi_gpu_step_drain(n):
     if gpu_count() < n:
         pytest.skip(f"needs {n} GPUs")
     assert _torchrun(n, "--suite", "drain", "--seeds", "0:12") == 0
+
+
+@pytest.mark.parametrize("n", [2, 4, 8])
+def test_multi_gpu_large_tables(n):
+    """W > 64 bitvectors across ranks (T = 4,096 random groups, T = 65,536 cfg4 groups of 8 with
+    rank-rotated orders): A words, released lists and values bit-exact, replicas identical."""
+    if gpu_count() < n:
+        pytest.skip(f"needs {n} GPUs")
+    assert _torchrun(n, "--suite", "bigT", "--seeds", "0:1", "--buffers", "f16") == 0
 
 
 @pytest.mark.parametrize("n", [2, 4, 8])
