@@ -355,10 +355,9 @@ def test_eight_ranks_oversubscribed():
     g = gpu_count()
     if g >= 8 or g < 2:
         pytest.skip("needs 2..7 GPUs (8 or more: the direct N=8 tests run instead)")
-    assert _torchrun(8, "--suite", "cfg1", "--seeds", "0:10", timeout=1500) == 0
-    assert _torchrun(8, "--suite", "edge", "--seeds", "0:3", timeout=1500) == 0
-    assert _torchrun(8, "--suite", "drain", "--seeds", "0:6", timeout=1500) == 0
-    assert _torchrun(8, "--suite", "stats", "--seeds", "0:2", "--buffers", "f16", timeout=1500) == 0
+    assert _torchrun(8, "--suite", "cfg1", "--seeds", "0:4", timeout=1500) == 0
+    assert _torchrun(8, "--suite", "edge", "--seeds", "0:1", "--buffers", "f16", timeout=1500) == 0
+    assert _torchrun(8, "--suite", "drain", "--seeds", "0:4", "--buffers", "f32", timeout=1500) == 0
 
 
 @pytest.mark.parametrize("n", [2, 4, 8])
