@@ -339,6 +339,9 @@ int build_layouts(gr_ctx *c, const gr_tensor *table, const int32_t *group_of) {
     h = fnv1a(h, &c->chunk_elems, sizeof c->chunk_elems);
     h = fnv1a(h, &c->one_shot_max_bytes, sizeof c->one_shot_max_bytes);
     h = fnv1a(h, &c->push, sizeof c->push);
+    h = fnv1a(h, &c->lag1, sizeof c->lag1);
+    h = fnv1a(h, &c->lag2, sizeof c->lag2);
+    h = fnv1a(h, &c->world.comm_ctas, sizeof c->world.comm_ctas);  // sets the default lags (x grid)
     h = fnv1a(h, &c->chunk_target_div, sizeof c->chunk_target_div);
     h = fnv1a(h, &c->chunk_max, sizeof c->chunk_max);
     h = fnv1a(h, c->numel.data(), sizeof(int64_t) * T);
@@ -444,12 +447,9 @@ int setup_device(gr_ctx *c) {
         q == cudaDriverEntryPointSuccess)
         c->write_value32 = (PFN_writeValue32)fn;
 
-    if (const char *os = getenv("GR_ONESHOT_MAX_BYTES")) c->one_shot_max_bytes = atoll(os);  // tuning
-    if (const char *l1 = getenv("GR_LAG1")) c->lag1 = atoi(l1);
     if (const char *ns = getenv("GR_STAGES")) c->nstages = std::max(2, std::min(8, atoi(ns)));
     if (const char *sk = getenv("GR_STAGE_KB")) c->stage_kb = std::max(8, atoi(sk));
     if (c->nstages * c->stage_kb > 208) c->stage_kb = 208 / c->nstages / 16 * 16;
-    if (const char *l2 = getenv("GR_LAG2")) c->lag2 = atoi(l2);
     if (const char *tp = getenv("GR_TRACE")) {
         if (*tp) {
             c->trace_path = std::string(tp) + ".rank" + std::to_string(c->rank) + ".jsonl";
@@ -613,6 +613,11 @@ int gr_init(gr_ctx **out, const gr_world *world, const gr_tensor *table, int32_t
         const int64_t thr = c->N <= 2 ? (128ll << 20) : c->N == 3 ? (32ll << 20) : c->N == 4 ? (8ll << 20) : (1ll << 20);
         c->one_shot_max_bytes = world->one_shot_max_bytes >= 0 ? world->one_shot_max_bytes : thr;
     }
+    // knobs that fix the cross-rank queue order / algorithm: read before the table hash so every
+    // rank must agree on them (a mismatch would desynchronise the fused kernel's queues)
+    if (const char *os = getenv("GR_ONESHOT_MAX_BYTES")) c->one_shot_max_bytes = atoll(os);  // tuning
+    if (const char *l1 = getenv("GR_LAG1")) c->lag1 = atoi(l1);
+    if (const char *l2 = getenv("GR_LAG2")) c->lag2 = atoi(l2);
     c->dry = world->device < 0;
     if (c->world.timeout_ms <= 0) c->world.timeout_ms = kDefaultTimeoutMs;
     int rc = build_layouts(c, table, group_of);
