@@ -114,11 +114,14 @@ def _rank_main(rank, port, mismatch, q):
     dist.init_process_group("gloo", rank=rank, world_size=2)
     from paper_1909_11150_b200 import Context, GrError, make_allgather
     numel = [100, 200, 300]
-    if mismatch and rank == 1:
+    comm_ctas = 0
+    if mismatch == "table" and rank == 1:
         numel = [100, 200, 301]
+    if mismatch == "queue" and rank == 1:
+        comm_ctas = 32  # sets the fused kernel's default queue lags: must agree across ranks
     try:
         ctx = Context(rank=rank, world_size=2, device=-1, numel=numel, group_of=[0, 1, 1],
-                      allgather=make_allgather(None))
+                      comm_ctas=comm_ctas, allgather=make_allgather(None))
         q.put((rank, "ok", ctx.bit_of(), ctx.buf_offsets()))
         ctx.gr_finalize()
     except GrError as e:
@@ -126,7 +129,7 @@ def _rank_main(rank, port, mismatch, q):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("mismatch", [False, True])
+@pytest.mark.parametrize("mismatch", [None, "table", "queue"])
 def test_gloo_world2_init_consistency(mismatch):
     """gr_init is collective: identical tables agree on the cache/layout;
     any difference makes gr_init fail with GR_EMISMATCH on every rank."""
