@@ -66,6 +66,19 @@ def test_dry_init_layout_matches_oracle_cache(orc):
         ctx.gr_finalize()
 
 
+@pytest.mark.parametrize("T", [2046, 2047, 4096, 65536])
+def test_dry_init_large_tables_match_oracle_cache(orc, T):
+    """The response cache at and beyond the inline-bitvector size (W = 64 at T = 2046) up to
+    cfg4's largest table: bit positions identical to the oracle's (reading R3)."""
+    from workloads.schedules import random_partition
+    rng = np.random.default_rng(T)
+    g = random_partition(T, max(1, T // 8), rng)
+    ctx = dry(np.ones(T, dtype=np.int64), g)
+    assert ctx.W == orc.words(T) == (T + 2 + 31) // 32
+    assert ctx.bit_of() == [int(x) for x in orc.bit_positions(g)]
+    ctx.gr_finalize()
+
+
 @pytest.mark.parametrize("numel,group_of", [
     ([1, 2], [0, 2]),        # group 1 empty
     ([1, 0], [0, 0]),        # numel 0
