@@ -101,6 +101,10 @@ def test_dry_init_rejects_bad_world():
         dry([8], [0], chunk_elems=12)
     with pytest.raises(GrError):
         dry([8], [0], world_size=2)  # no allgather callback for N > 1
+    with pytest.raises(GrError):
+        dry([8], [0], world_size=9)  # one NVSwitch domain: at most 8 ranks (gr.h)
+    with pytest.raises(GrError):
+        dry([8], [0], world_size=0)
 
 
 def test_dry_context_refuses_compute_calls():
