@@ -120,3 +120,16 @@ def test_contiguous_groups_cover_in_reverse_order():
     assert sorted(set(g)) == [0, 1, 2]
     rev = [g[t] for t in reversed(range(len(numels)))]
     assert rev == sorted(rev)  # group ids ascend in backward (reverse registration) order
+
+
+@pytest.mark.parametrize("numels,n_groups", [([5], 4), ([1, 1], 8), ([10] * 7, 3), ([1, 1000, 1, 1], 2),
+                                             ([3, 3, 3, 3, 3, 3, 3, 3], 8)])
+def test_contiguous_groups_edge_cases(numels, n_groups):
+    """Dense ids 0..G-1 (G <= min(T, n_groups)), every group non-empty and contiguous in the
+    backward (reverse registration) order, ids ascending in that order."""
+    g = contiguous_groups(numels, n_groups)
+    T = len(numels)
+    G = len(set(g))
+    assert sorted(set(g)) == list(range(G)) and 1 <= G <= min(T, n_groups)
+    rev = [g[t] for t in reversed(range(T))]
+    assert rev == sorted(rev)
