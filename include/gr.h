@@ -107,6 +107,8 @@ typedef struct gr_ctx gr_ctx;
  *   world     [in]  see gr_world.
  *   table     [in]  T tensor descriptors (host, copied).
  *   group_of  [in]  group id per tensor, dense 0..G-1, every group non-empty (host, copied).
+ * Limits: T up to ~131,000 tensors (the bitvector kernel's 64 KB of shared memory holds
+ * 3 W words + ceil(G/32) words; GR_EINVAL beyond).
  * Errors: GR_EINVAL, GR_EMISMATCH (a hash of all of the above differs on some
  * rank; "globally consistent order"), GR_ECUDA, GR_ENOMEM.
  * With world->device < 0 the call only validates and builds the host-side

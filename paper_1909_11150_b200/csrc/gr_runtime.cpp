@@ -237,6 +237,13 @@ int build_layouts(gr_ctx *c, const gr_tensor *table, const int32_t *group_of) {
                      [&](int32_t a, int32_t b) { return group_of[a] < group_of[b]; });
     c->nbits = GR_STATUS_BITS + T;
     c->W = (c->nbits + 31) / 32;
+    {   // the bitvector kernel keeps L, A, released words and the complete-group mask in shared
+        // memory (64 KB opt-in): about 131,000 tensors at most
+        const size_t smem = sizeof(uint32_t) * (3 * (size_t)c->W + ((size_t)G + 31) / 32);
+        if (smem > 64 * 1024)
+            return fail(nullptr, GR_EINVAL, "%d tensors / %d groups exceed the bitvector kernel's 64 KB "
+                        "shared-memory budget (%zu B)", T, G, smem);
+    }
     c->bit_of.assign(T, 0);
     c->tensor_of_bit.assign((size_t)c->W * 32, -1);
     c->group_of_bit.assign((size_t)c->W * 32, -1);

@@ -107,6 +107,18 @@ def test_dry_init_rejects_bad_world():
         dry([8], [0], world_size=0)
 
 
+def test_dry_init_table_size_limit():
+    """T up to ~131K tensors (the bitvector kernel's 64 KB shared-memory budget: 3 W words plus
+    the complete-group mask); beyond, EINVAL. Singleton groups are the largest case."""
+    from paper_1909_11150_b200 import GrError
+    from paper_1909_11150_b200.binding import GR_EINVAL
+    ctx = dry(np.ones(131000, dtype=np.int64), np.arange(131000))
+    ctx.gr_finalize()
+    with pytest.raises(GrError) as e:
+        dry(np.ones(132000, dtype=np.int64), np.arange(132000))
+    assert e.value.code == GR_EINVAL
+
+
 def test_dry_context_refuses_compute_calls():
     from paper_1909_11150_b200 import GrError
     ctx = dry([8, 8], [0, 1])
