@@ -138,15 +138,20 @@ int gr_mark_ready_batch(gr_ctx *ctx, int32_t rank, int32_t n, const int32_t *ten
  * stream-ordered: the ready flag is written by `stream` (cudaStream_t) when
  * the work enqueued on it before this call has completed (a driver stream
  * memory operation), so a cycle sees the tensor only once its gradient really
- * exists. Used to overlap reduction with a still-running backward pass. */
+ * exists. Used to overlap reduction with a still-running backward pass.
+ * stream is borrowed for the call; dev_ptr until gr_wait returns.
+ * Errors: as gr_mark_ready, plus GR_ECUDA if the stream write cannot be enqueued. */
 int gr_mark_ready_async(gr_ctx *ctx, int32_t rank, int32_t tensor_id, void *dev_ptr,
                         void *stream);
 
 /* gr_step — COLLECTIVE: one coordination cycle ("tic").
- * Launches the bitvector kernel (populate with __ballot_sync, publish, AND
- * over N ranks through peer loads with __reduce_and_sync, group release),
- * waits for its result, and enqueues the fused pack -> sum-allreduce -> x1/N
- * -> unpack kernel for the released groups (asynchronous; gr_wait finishes it).
+ * Launches the bitvector kernel (populate: a thread per word from the host
+ * marks, or a __ballot_sync over the per-tensor flags of stream-ordered marks;
+ * publish; AND over N ranks through peer loads; group release, with
+ * __reduce_and_sync for groups spanning many words), enqueues the fused pack ->
+ * sum-allreduce -> x1/N -> unpack kernel behind it (it reads the released set
+ * from device memory, so the reduction starts the moment the bitvector kernel
+ * ends; gr_wait finishes it), and waits for the bitvector kernel's result.
  *   released     [out] host array, capacity >= G: released group ids, ascending.
  *   info         [out] host struct (nullable).
  *   global_bits  [out] host array of W u32 words receiving the intersected
