@@ -117,6 +117,23 @@ typedef struct gr_ctx gr_ctx;
 int gr_init(gr_ctx **out, const gr_world *world, const gr_tensor *table, int32_t T,
             const int32_t *group_of, int32_t G);
 
+/* gr_init_virtual — N ranks in ONE process on ONE device ("virtual ranks"; for testing and
+ * profiling the N-rank path on a single GPU). Creates out[0..N-1], N = world->world_size in
+ * 2..8, each an ordinary context of rank r with everything gr_init builds (response cache,
+ * layouts, its own symmetric memory, streams and epochs); a peer's memory is plain memory of
+ * the same device instead of a CUDA-IPC mapping, and NVLS is off. world->rank and
+ * world->allgather are ignored. Every other call works per rank as documented, with one
+ * rule: the collective calls (gr_step, gr_step_drain) of the N ranks must be made
+ * concurrently, one host thread per rank, as they would be by N processes — each rank's
+ * bitvector and reduction kernels are fired as ONE launch over all ranks (grid = ranks x
+ * CTAs, every CTA resident, floor(SMs / N) CTAs per rank), when the last rank arrives. A rank
+ * that has not arrived within timeout_ms is launched as absent: the others report
+ * GR_ETIMEOUT, as with a stalled peer process (SPEC.md:406 analogue).
+ *   out   [out] host array of world_size context pointers.
+ * Errors: as gr_init (no GR_EMISMATCH: one table); on error every out[r] is NULL. */
+int gr_init_virtual(gr_ctx **out, const gr_world *world, const gr_tensor *table, int32_t T,
+                    const int32_t *group_of, int32_t G);
+
 /* gr_mark_ready — LOCAL, thread-safe against a concurrent gr_step.
  * §4.1 step 1's "pending request": tensor tensor_id of this rank is ready and
  * its gradient lives at dev_ptr (device memory, numel elements of grad_dtype,

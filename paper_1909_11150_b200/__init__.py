@@ -16,4 +16,5 @@ from .binding import (  # noqa: F401
     GR_ALGO_TWOSHOT,
     gr_bench_spin,
     make_allgather,
+    virtual_world,
 )

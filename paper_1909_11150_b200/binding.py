@@ -63,6 +63,7 @@ def _load():
     p, i32, i64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64
     sig = {
         "gr_init": ([ctypes.POINTER(p), ctypes.POINTER(GrWorld), ctypes.POINTER(GrTensor), i32, p, i32], ctypes.c_int),
+        "gr_init_virtual": ([p, ctypes.POINTER(GrWorld), ctypes.POINTER(GrTensor), i32, p, i32], ctypes.c_int),
         "gr_mark_ready": ([p, i32, i32, p], ctypes.c_int),
         "gr_mark_ready_async": ([p, i32, i32, p, p], ctypes.c_int),
         "gr_mark_ready_batch": ([p, i32, i32, p, p], ctypes.c_int),
@@ -89,7 +90,7 @@ def _load():
 
 
 lib = _load()
-EXPORTED = ("gr_init", "gr_mark_ready", "gr_mark_ready_batch", "gr_mark_ready_async", "gr_step", "gr_wait", "gr_wait_async", "gr_released_wait_async", "gr_step_drain", "gr_set_status",
+EXPORTED = ("gr_init", "gr_init_virtual", "gr_mark_ready", "gr_mark_ready_batch", "gr_mark_ready_async", "gr_step", "gr_wait", "gr_wait_async", "gr_released_wait_async", "gr_step_drain", "gr_set_status",
             "gr_finalize", "gr_last_error", "gr_query", "gr_set_timing", "gr_reset_stats", "gr_bench_spin",
             "gr_enable_grad_stats", "gr_grad_stats")
 
@@ -124,26 +125,33 @@ def make_allgather(pg=None, device=None):
     return ALLGATHER_FN(cb)
 
 
+def _tables(numel, group_of, grad_f16):
+    T = len(numel)
+    tab = (GrTensor * T)()
+    for t in range(T):
+        tab[t].numel = int(numel[t])
+        tab[t].grad_dtype = GR_F16 if (grad_f16 is not None and grad_f16[t]) else GR_F32
+    grp = (ctypes.c_int32 * T)(*[int(g) for g in group_of])
+    return T, int(max(group_of)) + 1, tab, grp
+
+
 class Context:
     """Owns one gr_ctx; methods map 1:1 onto the C calls."""
 
     def __init__(self, *, rank: int, world_size: int, device: int, numel, group_of, grad_f16=None,
                  buffer_dtype: int = GR_F16, compute_stream: int = 0, one_shot_max_bytes: int = -1,
-                 timeout_ms: int = 0, comm_ctas: int = 0, chunk_elems: int = 0, allgather=None):
-        T = len(numel)
-        self.T = T
-        self.G = int(max(group_of)) + 1
-        tab = (GrTensor * T)()
-        for t in range(T):
-            tab[t].numel = int(numel[t])
-            tab[t].grad_dtype = GR_F16 if (grad_f16 is not None and grad_f16[t]) else GR_F32
-        grp = (ctypes.c_int32 * T)(*[int(g) for g in group_of])
-        self._allgather = allgather if allgather is not None else ALLGATHER_FN()
-        w = GrWorld(rank, world_size, device, compute_stream, buffer_dtype, one_shot_max_bytes, timeout_ms,
-                    comm_ctas, chunk_elems, self._allgather, None)
-        self._ctx = ctypes.c_void_p()
-        rc = lib.gr_init(ctypes.byref(self._ctx), ctypes.byref(w), tab, T, ctypes.cast(grp, ctypes.c_void_p), self.G)
-        _check(rc, None)
+                 timeout_ms: int = 0, comm_ctas: int = 0, chunk_elems: int = 0, allgather=None, _handle=None):
+        T, G, tab, grp = _tables(numel, group_of, grad_f16)
+        self.T, self.G = T, G
+        if _handle is not None:  # one rank of gr_init_virtual (virtual_world)
+            self._ctx = ctypes.c_void_p(_handle)
+        else:
+            self._allgather = allgather if allgather is not None else ALLGATHER_FN()
+            w = GrWorld(rank, world_size, device, compute_stream, buffer_dtype, one_shot_max_bytes, timeout_ms,
+                        comm_ctas, chunk_elems, self._allgather, None)
+            self._ctx = ctypes.c_void_p()
+            rc = lib.gr_init(ctypes.byref(self._ctx), ctypes.byref(w), tab, T, ctypes.cast(grp, ctypes.c_void_p), G)
+            _check(rc, None)
         self.rank = rank
         self.W = self.query_int(GR_Q_WORDS)
         self._released = (ctypes.c_int32 * self.G)()
@@ -259,6 +267,22 @@ class Context:
             self.gr_finalize()
         except Exception:
             pass
+
+
+def virtual_world(*, world_size: int, device: int, numel, group_of, grad_f16=None, buffer_dtype: int = GR_F16,
+                  compute_stream: int = 0, one_shot_max_bytes: int = -1, timeout_ms: int = 0, comm_ctas: int = 0,
+                  chunk_elems: int = 0):
+    """gr_init_virtual: world_size ranks on one device, one Context per rank. Their collective
+    calls (gr_step, gr_step_drain) must be made concurrently, one thread per rank (ctypes
+    releases the GIL during the call)."""
+    T, G, tab, grp = _tables(numel, group_of, grad_f16)
+    w = GrWorld(0, world_size, device, compute_stream, buffer_dtype, one_shot_max_bytes, timeout_ms, comm_ctas,
+                chunk_elems, ALLGATHER_FN(), None)
+    outs = (ctypes.c_void_p * world_size)()
+    _check(lib.gr_init_virtual(ctypes.cast(outs, ctypes.c_void_p), ctypes.byref(w), tab, T,
+                               ctypes.cast(grp, ctypes.c_void_p), G), None)
+    return [Context(rank=r, world_size=world_size, device=device, numel=numel, group_of=group_of, grad_f16=grad_f16,
+                    _handle=outs[r]) for r in range(world_size)]
 
 
 def gr_bench_spin(ns: int, ctas: int, stream: int):

@@ -57,6 +57,9 @@ struct DevCycle {
 struct BvParams {
     const uint32_t *host_bits;       // device copy [W] of the host mark bits (DMA'd before the launch);
                                      // unused when W <= GR_BV_INLINE_WORDS (passed in inline_bits)
+    const uint32_t *marked_bits;     // device copy [W] of every mark taken by the cycle's snapshot:
+                                     // a stream-ordered flag counts only if its mark (and so its
+                                     // pointer) is in the snapshot; inline_marked when inline
     const uint32_t *dev_flags;       // device [W*32]: step epoch written by gr_mark_ready_async
     uint32_t *rel_words;             // device [W]: tensor bits released so far in this step
     int32_t new_step;                // 1 on the first cycle of a step (rel_words restart at 0)
@@ -85,7 +88,8 @@ struct BvParams {
     int32_t drain;                   // gr_step_drain: wait on the device until every unreleased
                                      // tensor of this rank is ready, no host hand-off awaited
     HostError *err;                  // drain only: failures surface here (host-mapped)
-    uint32_t inline_bits[GR_BV_INLINE_WORDS];  // snapshot of host_bits passed with the launch
+    uint32_t inline_bits[GR_BV_INLINE_WORDS];    // snapshot of host_bits passed with the launch
+    uint32_t inline_marked[GR_BV_INLINE_WORDS];  // snapshot of marked_bits passed with the launch
 };
 
 enum Algo { ALGO_LOCAL = 1, ALGO_ONESHOT = 2, ALGO_TWOSHOT = 3, ALGO_NVLS = 4 };
@@ -133,8 +137,23 @@ struct DataParams {
     uint64_t timeout_ns;
 };
 
+// Virtual ranks (gr_init_virtual): every rank's parameters for one launch on one device.
+// Rank r with bit r of `absent` set never reached the launch (its CTAs exit at once).
+struct BvParamsV {
+    BvParams r[GR_MAX_RANKS];
+    int32_t N;
+    uint32_t absent;
+};
+struct DataParamsV {
+    DataParams r[GR_MAX_RANKS];
+    int32_t N, per;                    // ranks, CTAs per rank (grid = N * per)
+    uint32_t absent;
+};
+
 // Kernel launchers (gr_kernels.cu). Return cudaError_t as int.
 int launch_bitvector(const BvParams &p, void *stream);
+int launch_bitvector_virtual(const BvParamsV &pv, void *stream);
+int launch_data_virtual(const DataParamsV &pv, int buffer_f16, int stats, void *stream);
 int launch_data(const DataParams &p, int local, int buffer_f16, int ctas, void *stream);
 int data_kernel_max_ctas(int algo, int buffer_f16, int *out);
 int launch_spin(int64_t ns, int ctas, void *stream);

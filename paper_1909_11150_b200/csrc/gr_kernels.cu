@@ -80,7 +80,7 @@ constexpr int BV_BATCH = GR_BV_BATCH;
 // Two instantiations: 256 threads (small bitvectors; 56 registers, co-resident with a running
 // reduction) and 1024 threads (W > 64 words, i.e. more than ~2000 tensors).
 template <int NT>
-__global__ void __launch_bounds__(NT, 1024 / NT) bitvector_kernel(BvParams p) {
+__device__ __forceinline__ void bitvector_body(const BvParams &p) {
     extern __shared__ uint32_t smem[];
     const int W = p.W, G = p.G, Gw = (p.G + 31) / 32;
     uint32_t *sL = smem, *sA = smem + W, *sR = smem + 2 * W, *sC = smem + 3 * W;
@@ -115,19 +115,21 @@ __global__ void __launch_bounds__(NT, 1024 / NT) bitvector_kernel(BvParams p) {
         }
     }
     for (int w0 = warp; p.check_async && w0 < W; w0 += nwarps * BV_BATCH) {
-        uint32_t f[BV_BATCH], hb[BV_BATCH];
+        uint32_t f[BV_BATCH], hb[BV_BATCH], mk[BV_BATCH];
 #pragma unroll
         for (int k = 0; k < BV_BATCH; ++k) {  // issue the independent loads first
             const int w = w0 + k * nwarps;
             const int b = w * 32 + lane;
             f[k] = (p.check_async && w < W && b >= GR_STATUS_BITS && b < p.nbits) ? ld_relaxed_sys32(p.dev_flags + b) : 0u;
             hb[k] = (w < W) ? (p.use_inline ? p.inline_bits[w] : p.host_bits[w]) : 0u;
+            mk[k] = (w < W) ? (p.use_inline ? p.inline_marked[w] : p.marked_bits[w]) : 0u;
         }
 #pragma unroll
         for (int k = 0; k < BV_BATCH; ++k) {
             const int w = w0 + k * nwarps;
             if (w >= W) break;  // warp-uniform
-            uint32_t ready = hb[k] | __ballot_sync(0xffffffffu, f[k] == p.epoch);
+            // a flag from a mark that raced past the cycle's snapshot waits for the next cycle
+            uint32_t ready = (hb[k] | __ballot_sync(0xffffffffu, f[k] == p.epoch)) & mk[k];
             const int lo = (w == 0) ? GR_STATUS_BITS : 0;                 // tensor bits of word w
             const int hi = min(32, p.nbits - w * 32);
             const uint32_t valid = (hi >= 32 ? 0xffffffffu : ((1u << hi) - 1u)) & ~((1u << lo) - 1u);
@@ -143,7 +145,7 @@ __global__ void __launch_bounds__(NT, 1024 / NT) bitvector_kernel(BvParams p) {
                     __nanosleep(backoff);
                     backoff = backoff < 2048 ? 2 * backoff : 2048;
                     const uint32_t fv = (b >= GR_STATUS_BITS && b < p.nbits) ? ld_relaxed_sys32(p.dev_flags + b) : 0u;
-                    ready = hb[k] | __ballot_sync(0xffffffffu, fv == p.epoch);
+                    ready = (hb[k] | __ballot_sync(0xffffffffu, fv == p.epoch)) & mk[k];
                 }
             }
             uint32_t word = ready & valid & ~sR[w];
@@ -339,6 +341,22 @@ __global__ void __launch_bounds__(NT, 1024 / NT) bitvector_kernel(BvParams p) {
     }
 }
 
+// One rank per launch (the product path: one process per GPU).
+template <int NT>
+__global__ void __launch_bounds__(NT, 1024 / NT) bitvector_kernel(const __grid_constant__ BvParams p) {
+    bitvector_body<NT>(p);
+}
+
+// Virtual ranks (gr_init_virtual): N ranks of one device in ONE launch, CTA r = rank r, so
+// every rank's CTA is resident while it spins on its peers' LL words. A rank that never
+// reached the launch (host barrier timed out) is `absent`: its CTA exits and its peers time
+// out on its words, as they would on a stalled process.
+template <int NT>
+__global__ void __launch_bounds__(NT, 1024 / NT) bitvector_kernel_v(const __grid_constant__ BvParamsV pv) {
+    if (blockIdx.x >= (unsigned)pv.N || ((pv.absent >> blockIdx.x) & 1u)) return;
+    bitvector_body<NT>(pv.r[blockIdx.x]);
+}
+
 // cudaFuncSetAttribute is per device: remember, per function, the devices it was set on
 // (thread-safe; a process may drive several GPUs)
 static bool first_use_on_device(std::atomic<uint64_t> &mask) {
@@ -348,15 +366,30 @@ static bool first_use_on_device(std::atomic<uint64_t> &mask) {
     return (mask.fetch_or(bit) & bit) == 0;
 }
 
-int launch_bitvector(const BvParams &p, void *stream) {
-    const size_t smem = sizeof(uint32_t) * (3 * (size_t)p.W + ((size_t)p.G + 31) / 32);
+static void bitvector_attrs() {
     static std::atomic<uint64_t> done{0};
     if (first_use_on_device(done)) {
         cudaFuncSetAttribute(bitvector_kernel<BV_THREADS>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
         cudaFuncSetAttribute(bitvector_kernel<1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+        cudaFuncSetAttribute(bitvector_kernel_v<BV_THREADS>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+        cudaFuncSetAttribute(bitvector_kernel_v<1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
     }
+}
+
+int launch_bitvector(const BvParams &p, void *stream) {
+    const size_t smem = sizeof(uint32_t) * (3 * (size_t)p.W + ((size_t)p.G + 31) / 32);
+    bitvector_attrs();
     if (p.W > GR_BV_INLINE_WORDS) bitvector_kernel<1024><<<1, 1024, smem, (cudaStream_t)stream>>>(p);
     else bitvector_kernel<BV_THREADS><<<1, BV_THREADS, smem, (cudaStream_t)stream>>>(p);
+    return (int)cudaGetLastError();
+}
+
+int launch_bitvector_virtual(const BvParamsV &pv, void *stream) {
+    const BvParams &p = pv.r[0];  // W and G are the same on every rank (one table)
+    const size_t smem = sizeof(uint32_t) * (3 * (size_t)p.W + ((size_t)p.G + 31) / 32);
+    bitvector_attrs();
+    if (p.W > GR_BV_INLINE_WORDS) bitvector_kernel_v<1024><<<pv.N, 1024, smem, (cudaStream_t)stream>>>(pv);
+    else bitvector_kernel_v<BV_THREADS><<<pv.N, BV_THREADS, smem, (cudaStream_t)stream>>>(pv);
     return (int)cudaGetLastError();
 }
 
@@ -555,7 +588,7 @@ struct GradStat {
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
         const unsigned anynf = __reduce_or_sync(0xffffffffu, nf);
-        if ((threadIdx.x & 31) == 0) {
+        if ((threadIdx.x & 31) == 0 && sumsq) {  // null: a virtual rank without statistics
             if (v != 0.0) atomicAdd(sumsq + tensor, v);
             if (anynf) atomicOr(nonfinite, 1);
         }
@@ -590,7 +623,7 @@ constexpr int LC_THREADS = 256;
 constexpr int LC_UNROLL = 2;
 
 template <typename BT, bool STATS>
-__global__ void __launch_bounds__(LC_THREADS, 3) local_kernel(DataParams p) {
+__global__ void __launch_bounds__(LC_THREADS, 3) local_kernel(const __grid_constant__ DataParams p) {
     using B = Buf<BT>;
     const int lane = threadIdx.x & 31;
     const int gw = blockIdx.x * (LC_THREADS / 32) + (threadIdx.x >> 5);
@@ -930,7 +963,7 @@ constexpr int XF_RCACHE = 512;  // released groups cached in shared memory for i
 // bitvector kernel (256 threads), so the next cycle's coordination never queues behind
 // a long reduction.
 template <typename BT, bool STATS>
-__global__ void __maxnreg__(96) xfer_kernel(DataParams p) {
+__device__ __forceinline__ void xfer_body(const DataParams &p, const int cta, const int nctas) {
     using B = Buf<BT>;
     extern __shared__ __align__(1024) char xsm[];
     __shared__ __align__(8) uint64_t full[XF_STAGES], empty[XF_STAGES];
@@ -1138,7 +1171,7 @@ __global__ void __maxnreg__(96) xfer_kernel(DataParams p) {
             meta[stage].kind = K_STOP;
             mbar_arrive(&full[stage]);
             if (p.trace) {  // per-CTA stall profile after the item stamps
-                uint64_t *pr = p.trace + (size_t)3 * p.trace_items + (size_t)blockIdx.x * 8;
+                uint64_t *pr = p.trace + (size_t)3 * p.trace_items + (size_t)cta * 8;
                 pr[0] = (uint64_t)(clock64() - prof_t0);
                 pr[1] = (uint64_t)prof_empty;
                 pr[2] = (uint64_t)prof_flags;
@@ -1221,13 +1254,13 @@ __global__ void __maxnreg__(96) xfer_kernel(DataParams p) {
                 uint32_t smid;
                 asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
                 p.trace[(size_t)item * 4 + 2] = globaltimer();
-                p.trace[(size_t)item * 4 + 3] = (uint64_t)blockIdx.x | ((uint64_t)smid << 32);
+                p.trace[(size_t)item * 4 + 3] = (uint64_t)cta | ((uint64_t)smid << 32);
             }
             if (++stage == nst) { stage = 0; ph ^= 1; }
         }
         publish(K_STOP, 0);
         if (p.trace && ct == 0) {
-            uint64_t *pr = p.trace + (size_t)3 * p.trace_items + (size_t)blockIdx.x * 8;
+            uint64_t *pr = p.trace + (size_t)3 * p.trace_items + (size_t)cta * 8;
             pr[3] = (uint64_t)(clock64() - prof_t0);
             pr[4] = (uint64_t)prof_full;
             pr[5] = (uint64_t)prof_flag;
@@ -1236,7 +1269,7 @@ __global__ void __maxnreg__(96) xfer_kernel(DataParams p) {
     __syncthreads();
     if (tid == 0) {
         __threadfence();
-        if (atomicAdd(p.done_counter, 1) == (int)gridDim.x - 1) {
+        if (atomicAdd(p.done_counter, 1) == nctas - 1) {
             *p.work_counter = 0;
             *p.done_counter = 0;
             __threadfence();
@@ -1245,10 +1278,33 @@ __global__ void __maxnreg__(96) xfer_kernel(DataParams p) {
 }
 
 template <typename BT, bool STATS>
-static int launch_data_t(const DataParams &p, int local, int ctas, cudaStream_t s) {
+__global__ void __maxnreg__(96) xfer_kernel(const __grid_constant__ DataParams p) {
+    xfer_body<BT, STATS>(p, blockIdx.x, gridDim.x);
+}
+
+// Virtual ranks: N ranks' reductions in ONE launch of N x per CTAs (one CTA per SM, so every
+// CTA is resident: the launch fits the SM count). CTAs are dealt round-robin (CTA b serves
+// rank b mod N), so any resident prefix of the grid holds CTAs of every rank; each rank's
+// CTAs share that rank's work queue exactly as a real rank's grid does.
+template <typename BT, bool STATS>
+__global__ void __maxnreg__(96) xfer_kernel_v(const __grid_constant__ DataParamsV pv) {
+    const int r = blockIdx.x % pv.N;
+    if ((pv.absent >> r) & 1u) return;
+    xfer_body<BT, STATS>(pv.r[r], blockIdx.x / pv.N, pv.per);
+}
+
+template <typename BT, bool STATS>
+static void xfer_attrs() {
     static std::atomic<uint64_t> done{0};
-    if (first_use_on_device(done))
+    if (first_use_on_device(done)) {
         cudaFuncSetAttribute(xfer_kernel<BT, STATS>, cudaFuncAttributeMaxDynamicSharedMemorySize, 208 * 1024);
+        cudaFuncSetAttribute(xfer_kernel_v<BT, STATS>, cudaFuncAttributeMaxDynamicSharedMemorySize, 208 * 1024);
+    }
+}
+
+template <typename BT, bool STATS>
+static int launch_data_t(const DataParams &p, int local, int ctas, cudaStream_t s) {
+    xfer_attrs<BT, STATS>();
     if (local) local_kernel<BT, STATS><<<ctas, LC_THREADS, 0, s>>>(p);
     else xfer_kernel<BT, STATS><<<ctas, XF_THREADS, (size_t)p.nstages * p.stage_bytes, s>>>(p);
     return (int)cudaGetLastError();
@@ -1258,6 +1314,19 @@ int launch_data(const DataParams &p, int local, int buffer_f16, int ctas, void *
     cudaStream_t s = (cudaStream_t)stream;
     if (p.sumsq) return buffer_f16 ? launch_data_t<__half, true>(p, local, ctas, s) : launch_data_t<float, true>(p, local, ctas, s);
     return buffer_f16 ? launch_data_t<__half, false>(p, local, ctas, s) : launch_data_t<float, false>(p, local, ctas, s);
+}
+
+template <typename BT, bool STATS>
+static int launch_data_v_t(const DataParamsV &pv, cudaStream_t s) {
+    xfer_attrs<BT, STATS>();
+    xfer_kernel_v<BT, STATS><<<pv.N * pv.per, XF_THREADS, (size_t)pv.r[0].nstages * pv.r[0].stage_bytes, s>>>(pv);
+    return (int)cudaGetLastError();
+}
+
+int launch_data_virtual(const DataParamsV &pv, int buffer_f16, int stats, void *stream) {
+    cudaStream_t s = (cudaStream_t)stream;
+    if (stats) return buffer_f16 ? launch_data_v_t<__half, true>(pv, s) : launch_data_v_t<float, true>(pv, s);
+    return buffer_f16 ? launch_data_v_t<__half, false>(pv, s) : launch_data_v_t<float, false>(pv, s);
 }
 
 template <typename BT>

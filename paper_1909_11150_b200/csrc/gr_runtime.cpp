@@ -15,6 +15,7 @@
 #include <fstream>
 #include <atomic>
 #include <chrono>
+#include <condition_variable>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -50,6 +51,36 @@ uint64_t fnv1a(uint64_t h, const void *data, size_t n) {
 
 typedef CUresult (*PFN_writeValue32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
 
+constexpr int kPtrStages = 4;  // pinned snapshots of the pointer table in flight (DMA sources)
+
+// Virtual ranks (gr_init_virtual): N contexts of ONE process on ONE device, each an ordinary
+// rank of the library (own marks, streams, symmetric memory, epochs), whose peers' memory is
+// plain device memory of the same GPU. The two cross-rank kernels of a cycle (bitvector, data)
+// must have every rank's CTAs resident at once, so each rank's launch is deposited here and
+// the last rank to arrive fires ONE launch covering all ranks (grid = ranks x CTAs) on the
+// group's stream; every rank's own stream waits for it. The collective calls (gr_step,
+// gr_step_drain) are therefore called concurrently, one thread per virtual rank, as ranks are
+// processes in the real deployment. A rank that does not arrive within timeout_ms is launched
+// as `absent` (its CTAs exit): its peers then time out on the device exactly as they would on
+// a stalled process (GR_ETIMEOUT).
+struct VPhase {
+    uint64_t gen = 0;              // launches fired so far
+    uint32_t arrived = 0;          // ranks deposited for launch `gen`
+    gr::BvParams bv[GR_MAX_RANKS];
+    gr::DataParams dp[GR_MAX_RANKS];
+    cudaEvent_t ev_in[GR_MAX_RANKS] = {};
+    cudaEvent_t ev_out[4] = {};    // per generation (mod 4): the fired launch
+    int rc[4] = {0, 0, 0, 0};
+};
+struct VGroup {
+    int N = 0, dev = -1, per = 1, buf_f16 = 1, refs = 0;
+    int32_t timeout_ms = 20000;
+    std::mutex mu;
+    std::condition_variable cv;
+    cudaStream_t stream[2] = {nullptr, nullptr};  // 0: bitvector launches, 1: data launches
+    VPhase ph[2];
+};
+
 }  // namespace
 
 struct gr_ctx {
@@ -74,6 +105,10 @@ struct gr_ctx {
     int64_t buf_elems = 0;
     int64_t max_chunk = 0;  // longest chunk of the layout (elements)
     int32_t C = 0;
+
+    // virtual ranks (gr_init_virtual; null for a real rank)
+    VGroup *vg = nullptr;
+    cudaEvent_t ev_vin[2] = {nullptr, nullptr};
 
     // device state
     int dev = -1;
@@ -100,9 +135,19 @@ struct gr_ctx {
     gr::DevCycle *d_info_ring = nullptr;
     int32_t *d_counters = nullptr;  // [0] work, [1] done, [2] abort
     // pinned host-mapped
-    uint32_t *h_bits = nullptr;   // sync marks, by bit
+    uint32_t *h_bits = nullptr;   // sync marks, by bit (live: gr_mark_ready writes, under mu)
+    uint32_t *h_marked = nullptr; // every mark (host or stream-ordered), by bit (live, under mu)
     uint32_t *d_flags = nullptr;  // async marks (device memory), by bit
-    uint64_t *h_ptr = nullptr;
+    uint64_t *h_ptr = nullptr;    // gradient pointer table (live, under mu)
+    // snapshots taken under mu at gr_step, the DMA sources of the device copies (a queued copy
+    // reads its source when it runs, so it must never read the live tables): the mark bits per
+    // released-list ring slot ([2W]: host bits, marked bits; W > GR_BV_INLINE_WORDS only) and
+    // the pointer table in kPtrStages buffers, each guarded by an event
+    uint32_t *h_bits_stage = nullptr;
+    uint64_t *h_ptr_stage = nullptr;
+    cudaEvent_t ev_ptr_stage[kPtrStages] = {};
+    bool ptr_stage_pending[kPtrStages] = {};
+    int ptr_stage_next = 0;
     gr::HostResult *h_res = nullptr;
     gr::HostError *h_err = nullptr;
     uint32_t *d_hbits = nullptr;
@@ -358,16 +403,29 @@ int build_layouts(gr_ctx *c, const gr_tensor *table, const int32_t *group_of) {
     return GR_OK;
 }
 
-int allgather(gr_ctx *c, const void *send, void *recv, size_t bytes) {
-    if (c->N == 1) {
+// the init-time collective (gr_world.allgather); a failed callback leaves c's error text
+int allgather_w(const gr_world &w, gr_ctx *c, const void *send, void *recv, size_t bytes) {
+    if (w.world_size == 1) {
         memcpy(recv, send, bytes);
         return GR_OK;
     }
-    if (!c->world.allgather) return fail(c, GR_EINVAL, "world.allgather is required when world_size > 1");
-    if (c->world.allgather(send, recv, bytes, c->world.user) != 0)
-        return fail(c, GR_EINVAL, "allgather callback failed");
+    if (!w.allgather) return fail(c, GR_EINVAL, "world.allgather is required when world_size > 1");
+    if (w.allgather(send, recv, bytes, w.user) != 0) return fail(c, GR_EINVAL, "allgather callback failed");
     return GR_OK;
 }
+
+int allgather(gr_ctx *c, const void *send, void *recv, size_t bytes) {
+    return allgather_w(c->world, c, send, recv, bytes);
+}
+
+// Init-time agreement: every rank contributes its local status (0 or a gr_status) to one
+// allgather, so a rank whose local step failed still takes part in the collective and every
+// rank fails together instead of leaving its peers blocked in the next gather.
+struct InitVote {
+    int32_t rc;
+    int32_t pad;
+    uint64_t hash;
+};
 
 template <typename T>
 int upload(gr_ctx *c, T **dst, const std::vector<T> &src) {
@@ -377,7 +435,9 @@ int upload(gr_ctx *c, T **dst, const std::vector<T> &src) {
     return GR_OK;
 }
 
-int setup_device(gr_ctx *c) {
+// Local half of the device setup (no communication): streams, events, symmetric memory,
+// device tables, pinned blocks.
+int setup_local(gr_ctx *c) {
     CK(c, cudaSetDevice(c->dev));
     CK(c, cudaFree(nullptr));  // make sure the primary context exists
     int lo = 0, hi = 0;
@@ -391,6 +451,9 @@ int setup_device(gr_ctx *c) {
     CK(c, cudaEventCreateWithFlags(&c->ev_drain, cudaEventDisableTiming));
     CK(c, cudaEventCreateWithFlags(&c->ev_bv, cudaEventDisableTiming));
     for (int i = 0; i < GR_SLOT_RING; ++i) CK(c, cudaEventCreateWithFlags(&c->ring_ev[i], cudaEventDisableTiming));
+    for (int i = 0; i < kPtrStages; ++i) CK(c, cudaEventCreateWithFlags(&c->ev_ptr_stage[i], cudaEventDisableTiming));
+    if (c->vg)
+        for (int i = 0; i < 2; ++i) CK(c, cudaEventCreateWithFlags(&c->ev_vin[i], cudaEventDisableTiming));
 
     // symmetric memory: [LL bitvector slots 2 x W u64][flag pad 2 x (C*N + C) u32][fusion buffer 2 x E]
     const int esz = c->buf_f16 ? 2 : 4;
@@ -420,8 +483,9 @@ int setup_device(gr_ctx *c) {
     RC(upload(c, &c->d_big, c->big_groups));
     CK(c, cudaMalloc((void **)&c->d_relw, sizeof(uint32_t) * c->W));
     CK(c, cudaMemset(c->d_relw, 0, sizeof(uint32_t) * c->W));
-    CK(c, cudaMalloc((void **)&c->d_hbits_dev, sizeof(uint32_t) * c->W));
+    CK(c, cudaMalloc((void **)&c->d_hbits_dev, sizeof(uint32_t) * 2 * c->W));  // host bits, marked bits
     CK(c, cudaMalloc((void **)&c->d_ptr, sizeof(uint64_t) * c->T));
+    CK(c, cudaMemset(c->d_ptr, 0, sizeof(uint64_t) * c->T));
     CK(c, cudaMalloc((void **)&c->d_rel_ring, sizeof(int32_t) * GR_SLOT_RING * (size_t)c->G));
     CK(c, cudaMalloc((void **)&c->d_cum_ring, sizeof(int32_t) * GR_SLOT_RING * (size_t)(c->G + 1)));
     CK(c, cudaMalloc((void **)&c->d_info_ring, sizeof(gr::DevCycle) * GR_SLOT_RING));
@@ -438,6 +502,11 @@ int setup_device(gr_ctx *c) {
     CK(c, cudaMemset(c->d_flags, 0, sizeof(uint32_t) * (size_t)c->W * 32));
     CK(c, cudaHostAlloc((void **)&c->h_ptr, sizeof(uint64_t) * c->T, hf));
     memset(c->h_ptr, 0, sizeof(uint64_t) * c->T);
+    CK(c, cudaHostAlloc((void **)&c->h_marked, sizeof(uint32_t) * (size_t)c->W, hf));
+    memset(c->h_marked, 0, sizeof(uint32_t) * (size_t)c->W);
+    CK(c, cudaHostAlloc((void **)&c->h_ptr_stage, sizeof(uint64_t) * c->T * kPtrStages, hf));
+    if (c->W > GR_BV_INLINE_WORDS)
+        CK(c, cudaHostAlloc((void **)&c->h_bits_stage, sizeof(uint32_t) * 2 * (size_t)c->W * GR_SLOT_RING, hf));
     c->res_bytes = sizeof(gr::HostResult) + sizeof(uint32_t) * c->W + sizeof(int32_t) * c->G;
     CK(c, cudaHostAlloc((void **)&c->h_res, c->res_bytes, hf));
     memset((void *)c->h_res, 0, c->res_bytes);
@@ -470,7 +539,8 @@ int setup_device(gr_ctx *c) {
     int sms = 0;
     CK(c, cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->dev));
     for (int algo = gr::ALGO_LOCAL; algo <= gr::ALGO_TWOSHOT; ++algo) {
-        int mx = sms;  // xfer kernel: one CTA per SM (shared-memory stage ring)
+        // xfer kernel: one CTA per SM (shared-memory stage ring); virtual ranks share the SMs
+        int mx = c->vg ? std::max(1, sms / c->N) : sms;
         int rc = algo == gr::ALGO_LOCAL ? gr::data_kernel_max_ctas(algo, c->buf_f16, &mx) : 0;
         if (rc != 0) return fail(c, GR_ECUDA, "occupancy query failed: %s", cudaGetErrorString((cudaError_t)rc));
         int want = c->world.comm_ctas > 0 ? c->world.comm_ctas : mx;
@@ -480,42 +550,65 @@ int setup_device(gr_ctx *c) {
         c->data_ctas_full[algo] = std::max(1, mx);
     }
     CK(c, cudaDeviceSynchronize());
+    return GR_OK;
+}
 
-    // exchange IPC handles; this allgather is also the barrier after zeroing the pads
-    cudaIpcMemHandle_t mine;
+// Whole device setup of a real rank: the local half, then the collective half. Every rank
+// enters each allgather whatever its local outcome (the status rides along), so a failure on
+// one rank fails gr_init on every rank instead of blocking the others.
+int setup_device(gr_ctx *c) {
+    struct IpcVote {
+        int32_t rc, pad;
+        cudaIpcMemHandle_t h;
+    } mine;
     memset(&mine, 0, sizeof mine);
-    if (c->N > 1) CK(c, cudaIpcGetMemHandle(&mine, c->symm));
-    std::vector<cudaIpcMemHandle_t> all(c->N);
-    int rc = allgather(c, &mine, all.data(), sizeof mine);
-    if (rc) return rc;
-    for (int r = 0; r < c->N; ++r) {
+    mine.rc = setup_local(c);
+    if (!mine.rc && c->N > 1) {
+        cudaError_t e = cudaIpcGetMemHandle(&mine.h, c->symm);
+        if (e != cudaSuccess) mine.rc = fail(c, GR_ECUDA, "cudaIpcGetMemHandle: %s", cudaGetErrorString(e));
+    }
+    const std::string local_err = c->err;
+    // exchange IPC handles; this allgather is also the barrier after zeroing the pads
+    std::vector<IpcVote> all(c->N);
+    RC(allgather(c, &mine, all.data(), sizeof mine));
+    for (int r = 0; r < c->N; ++r)
+        if (all[r].rc) {
+            if (mine.rc) return fail(c, mine.rc, "%s", local_err.c_str());
+            return fail(c, all[r].rc, "gr_init failed on rank %d (code %d)", r, all[r].rc);
+        }
+    int32_t open_rc = 0;
+    for (int r = 0; r < c->N && !open_rc; ++r) {
         if (r == c->rank) {
             c->peer_symm[r] = c->symm;
             continue;
         }
         void *p = nullptr;
-        CK(c, cudaIpcOpenMemHandle(&p, all[r], cudaIpcMemLazyEnablePeerAccess));
-        c->peer_symm[r] = (char *)p;
+        cudaError_t e = cudaIpcOpenMemHandle(&p, all[r].h, cudaIpcMemLazyEnablePeerAccess);
+        if (e != cudaSuccess) open_rc = fail(c, GR_ECUDA, "cudaIpcOpenMemHandle(rank %d): %s", r, cudaGetErrorString(e));
+        else c->peer_symm[r] = (char *)p;
     }
 
     // NVLS (NEXT-1): in-switch reduction for large messages. It moves S(1+1/N) NVLink bytes per
-    // direction against 2S(N-1)/N for two-shot; measured at N = 4 it is still slower than
-    // two-shot, so it defaults on only from N = 8. GR_NVLS=1 forces it from
-    // N = 2, GR_NVLS=0 turns it off.
+    // direction against 2S(N-1)/N for two-shot; measured at N = 4 it is slower than two-shot
+    // and it has not been measured at N = 8, so it is off unless GR_NVLS=1 asks
+    // for it (from N = 2). The vote also carries the peer-mapping status.
     if (c->N > 1) {
         const char *e = getenv("GR_NVLS");
-        const bool want = e ? atoi(e) != 0 : c->N >= 8;
+        const bool want = e ? atoi(e) != 0 : false;
         auto ag = [c](const void *snd, void *rcv, size_t n) { return allgather(c, snd, rcv, n); };
-        int32_t w = want ? 1 : 0;
-        std::vector<int32_t> ws(c->N);
-        RC(allgather(c, &w, ws.data(), sizeof w));
-        bool all = true;
-        for (int v : ws) all = all && v;
-        if (all) {
+        int32_t w[2] = {open_rc, want ? 1 : 0};
+        std::vector<int32_t> ws(2 * (size_t)c->N);
+        RC(allgather(c, w, ws.data(), sizeof w));
+        bool all_want = true;
+        for (int r = 0; r < c->N; ++r) {
+            if (ws[2 * r]) return open_rc ? open_rc : fail(c, ws[2 * r], "gr_init failed on rank %d (peer mapping)", r);
+            all_want = all_want && ws[2 * r + 1];
+        }
+        if (all_want) {
             if (gr::nvls_setup(c->nvls, c->rank, c->N, c->dev, 2 * c->buf_parity_bytes, ag, c->nvls_why) == 0)
                 c->nvls_why = "enabled";
         } else {
-            c->nvls_why = "disabled (GR_NVLS / world size)";
+            c->nvls_why = "disabled (default off; GR_NVLS=1 enables it)";
         }
     }
     return GR_OK;
@@ -527,7 +620,7 @@ void free_all(gr_ctx *c) {
     if (c->s_coord) cudaStreamSynchronize(c->s_coord);
     if (c->s_data) cudaStreamSynchronize(c->s_data);
     for (int r = 0; r < c->N; ++r)
-        if (r != c->rank && c->peer_symm[r]) cudaIpcCloseMemHandle(c->peer_symm[r]);
+        if (!c->vg && r != c->rank && c->peer_symm[r]) cudaIpcCloseMemHandle(c->peer_symm[r]);
     gr::nvls_free(c->nvls);
     cudaFree(c->symm);
     void *dptrs[] = {c->d_segs, c->d_chunks, c->d_cbeg, c->d_cend, c->d_gbb, c->d_gbe, c->d_gnch, c->d_gcb,
@@ -535,7 +628,14 @@ void free_all(gr_ctx *c) {
                      c->d_flags, c->d_trace, c->d_sumsq, c->d_nonfinite};
     for (void *p : dptrs) cudaFree(p);
     cudaFreeHost(c->h_bits);
+    cudaFreeHost(c->h_marked);
     cudaFreeHost(c->h_ptr);
+    cudaFreeHost(c->h_ptr_stage);
+    cudaFreeHost(c->h_bits_stage);
+    for (int i = 0; i < kPtrStages; ++i)
+        if (c->ev_ptr_stage[i]) cudaEventDestroy(c->ev_ptr_stage[i]);
+    for (int i = 0; i < 2; ++i)
+        if (c->ev_vin[i]) cudaEventDestroy(c->ev_vin[i]);
     cudaFreeHost((void *)c->h_res);
     cudaFreeHost((void *)c->h_err);
     for (int i = 0; i < GR_SLOT_RING; ++i)
@@ -552,6 +652,87 @@ void free_all(gr_ctx *c) {
         }
     if (c->s_coord) cudaStreamDestroy(c->s_coord);
     if (c->s_data) cudaStreamDestroy(c->s_data);
+    if (VGroup *g = c->vg) {  // the last virtual rank frees the group
+        c->vg = nullptr;
+        bool last;
+        {
+            std::lock_guard<std::mutex> lk(g->mu);
+            last = --g->refs == 0;
+        }
+        if (last) {
+            for (auto &s : g->stream)
+                if (s) {
+                    cudaStreamSynchronize(s);
+                    cudaStreamDestroy(s);
+                }
+            for (auto &ph : g->ph)
+                for (auto &e : ph.ev_out)
+                    if (e) cudaEventDestroy(e);
+            delete g;
+        }
+    }
+}
+
+// ---------------------------------------------------------------- virtual-rank launches
+// Deposit this rank's launch of `phase` (0 bitvector, 1 data) and take part in firing it; on
+// return `own` (the rank's stream) is ordered after the combined launch.
+int vg_launch(gr_ctx *c, int phase, cudaStream_t own, const gr::BvParams *bv, const gr::DataParams *dp) {
+    VGroup &g = *c->vg;
+    VPhase &ph = g.ph[phase];
+    CK(c, cudaEventRecord(c->ev_vin[phase], own));  // this rank's work before the launch
+    std::unique_lock<std::mutex> lk(g.mu);
+    const uint64_t my = ph.gen;
+    const uint32_t all = (1u << g.N) - 1u;
+    if (bv) ph.bv[c->rank] = *bv;
+    else ph.dp[c->rank] = *dp;
+    ph.ev_in[c->rank] = c->ev_vin[phase];
+    ph.arrived |= 1u << c->rank;
+    if (ph.arrived != all)
+        g.cv.wait_until(lk, std::chrono::steady_clock::now() + std::chrono::milliseconds(g.timeout_ms),
+                        [&] { return ph.gen != my; });
+    if (ph.gen == my) {  // last to arrive, or the others are late: fire with whoever is here
+        const int k = (int)(my & 3);
+        cudaStream_t s = g.stream[phase];
+        int rc = 0;
+        for (int r = 0; r < g.N && !rc; ++r)
+            if ((ph.arrived >> r) & 1u) rc = (int)cudaStreamWaitEvent(s, ph.ev_in[r], 0);
+        if (!rc) {
+            if (phase == 0) {
+                gr::BvParamsV pv{};
+                pv.N = g.N;
+                pv.absent = all & ~ph.arrived;
+                for (int r = 0; r < g.N; ++r)
+                    if ((ph.arrived >> r) & 1u) pv.r[r] = ph.bv[r];
+                rc = gr::launch_bitvector_virtual(pv, s);
+            } else {
+                gr::DataParamsV pv{};
+                pv.N = g.N;
+                pv.per = g.per;
+                pv.absent = all & ~ph.arrived;
+                int stats = 0;
+                for (int r = 0; r < g.N; ++r)
+                    if ((ph.arrived >> r) & 1u) {
+                        pv.r[r] = ph.dp[r];
+                        stats |= ph.dp[r].sumsq != nullptr;
+                    }
+                rc = gr::launch_data_virtual(pv, g.buf_f16, stats, s);
+            }
+        }
+        if (!rc) rc = (int)cudaEventRecord(ph.ev_out[k], s);
+        ph.rc[k] = rc;
+        ph.gen++;
+        ph.arrived = 0;
+        g.cv.notify_all();
+    }
+    const int k = (int)(my & 3);
+    const int rc = ph.rc[k];
+    cudaEvent_t ev = ph.ev_out[k];
+    lk.unlock();
+    if (rc) return fail(c, GR_ECUDA, "virtual-rank %s launch: %s", phase ? "data" : "bitvector",
+                        cudaGetErrorString((cudaError_t)rc));
+    // ev_out[k] is re-recorded only 4 launches later, which needs this rank again (or 4 timeouts)
+    CK(c, cudaStreamWaitEvent(own, ev, 0));
+    return GR_OK;
 }
 
 std::pair<cudaEvent_t, cudaEvent_t> get_ev_pair(gr_ctx *c) {
@@ -585,13 +766,13 @@ int collect_timing(gr_ctx *c) {
 
 extern "C" {
 
-int gr_init(gr_ctx **out, const gr_world *world, const gr_tensor *table, int32_t T, const int32_t *group_of,
-            int32_t G) {
-    if (!out || !world || !table || !group_of) return fail(nullptr, GR_EINVAL, "null argument to gr_init");
+// Local half of gr_init: validate the arguments and build the host-side layouts (no
+// communication). On error *out is null and g_init_error holds the text.
+static int create_ctx(gr_ctx **out, const gr_world *world, const gr_tensor *table, int32_t T,
+                      const int32_t *group_of, int32_t G) {
     *out = nullptr;
+    if (!table || !group_of) return fail(nullptr, GR_EINVAL, "null argument to gr_init");
     if (T <= 0 || G <= 0 || G > T) return fail(nullptr, GR_EINVAL, "need 0 < G <= T (T=%d, G=%d)", T, G);
-    if (world->world_size < 1 || world->world_size > GR_MAX_RANKS)
-        return fail(nullptr, GR_EINVAL, "world_size must be in 1..%d", GR_MAX_RANKS);
     if (world->rank < 0 || world->rank >= world->world_size) return fail(nullptr, GR_EINVAL, "bad rank");
     if (world->buffer_dtype != GR_F16 && world->buffer_dtype != GR_F32)
         return fail(nullptr, GR_EINVAL, "bad buffer dtype");
@@ -633,22 +814,45 @@ int gr_init(gr_ctx **out, const gr_world *world, const gr_tensor *table, int32_t
         return rc;
     }
     c->marked.assign(T, 0);
-    // global consistency check: every rank must have built the same cache
-    std::vector<uint64_t> hashes(c->N);
-    rc = allgather(c, &c->hash, hashes.data(), sizeof(uint64_t));
+    c->dev = c->dry ? -1 : world->device;
+    *out = c;
+    return GR_OK;
+}
+
+int gr_init(gr_ctx **out, const gr_world *world, const gr_tensor *table, int32_t T, const int32_t *group_of,
+            int32_t G) {
+    if (!out || !world) return fail(nullptr, GR_EINVAL, "null argument to gr_init");
+    *out = nullptr;
+    if (world->world_size < 1 || world->world_size > GR_MAX_RANKS)
+        return fail(nullptr, GR_EINVAL, "world_size must be in 1..%d", GR_MAX_RANKS);
+    gr_ctx *c = nullptr;
+    const int local_rc = create_ctx(&c, world, table, T, group_of, G);
+    const std::string local_err = g_init_error;
+    // global consistency check: every rank must have built the same cache. A rank
+    // whose arguments were rejected still takes part (its status rides along), so every rank
+    // returns instead of leaving the others blocked in the gather.
+    InitVote mine{local_rc, 0, c ? c->hash : 0};
+    std::vector<InitVote> votes(world->world_size);
+    gr_ctx tmp;
+    tmp.world = *world;
+    int rc = allgather_w(*world, &tmp, &mine, votes.data(), sizeof mine);
     if (rc) {
-        g_init_error = c->err;
         delete c;
-        return rc;
+        return fail(nullptr, rc, "%s", tmp.err.c_str());
     }
-    for (int r = 0; r < c->N; ++r)
-        if (hashes[r] != c->hash) {
+    for (int r = 0; r < world->world_size; ++r)
+        if (votes[r].rc) {
+            delete c;
+            if (local_rc) return fail(nullptr, local_rc, "%s", local_err.c_str());
+            return fail(nullptr, votes[r].rc, "gr_init failed on rank %d (code %d)", r, votes[r].rc);
+        }
+    for (int r = 0; r < world->world_size; ++r)
+        if (votes[r].hash != c->hash) {
             fail(nullptr, GR_EMISMATCH, "rank %d's tensor table / groups / config differ from rank %d's", r, c->rank);
             delete c;
             return GR_EMISMATCH;
         }
     if (!c->dry) {
-        c->dev = world->device;
         rc = setup_device(c);
         if (rc) {
             g_init_error = c->err;
@@ -658,6 +862,59 @@ int gr_init(gr_ctx **out, const gr_world *world, const gr_tensor *table, int32_t
         }
     }
     *out = c;
+    return GR_OK;
+}
+
+int gr_init_virtual(gr_ctx **out, const gr_world *world, const gr_tensor *table, int32_t T,
+                    const int32_t *group_of, int32_t G) {
+    if (!out || !world) return fail(nullptr, GR_EINVAL, "null argument to gr_init_virtual");
+    const int N = world->world_size;
+    if (N < 2 || N > GR_MAX_RANKS) return fail(nullptr, GR_EINVAL, "virtual world_size must be in 2..%d", GR_MAX_RANKS);
+    for (int r = 0; r < N; ++r) out[r] = nullptr;
+    if (world->device < 0) return fail(nullptr, GR_EINVAL, "virtual ranks need a device");
+    VGroup *g = new (std::nothrow) VGroup();
+    if (!g) return fail(nullptr, GR_ENOMEM, "out of host memory");
+    g->N = N;
+    g->dev = world->device;
+    g->buf_f16 = world->buffer_dtype == GR_F16;
+    g->timeout_ms = world->timeout_ms > 0 ? world->timeout_ms : kDefaultTimeoutMs;
+    auto undo = [&](int rc) {
+        std::string e = g_init_error;
+        bool any = false;
+        for (int r = 0; r < N; ++r)
+            if (out[r]) {
+                any = true;
+                if (out[r]->err != "no error") e = out[r]->err;
+                gr_finalize(out[r]);  // drops a group reference
+                out[r] = nullptr;
+            }
+        if (!any) delete g;
+        return fail(nullptr, rc, "%s", e.c_str());
+    };
+    for (int r = 0; r < N; ++r) {
+        gr_world w = *world;
+        w.rank = r;
+        w.allgather = nullptr;  // the ranks live in this process: nothing to gather
+        gr_ctx *c = nullptr;
+        int rc = create_ctx(&c, &w, table, T, group_of, G);
+        if (rc) return undo(rc);
+        c->vg = g;
+        g->refs++;
+        out[r] = c;
+        rc = setup_local(c);
+        if (rc) return undo(rc);
+        c->nvls_why = "disabled (virtual ranks share one device)";
+    }
+    for (int r = 0; r < N; ++r)
+        for (int q = 0; q < N; ++q) out[r]->peer_symm[q] = out[q]->symm;
+    g->per = out[0]->data_ctas[gr::ALGO_TWOSHOT];
+    int lo = 0, hi = 0;
+    if (cudaDeviceGetStreamPriorityRange(&lo, &hi) != cudaSuccess) return undo(GR_ECUDA);
+    for (auto &s : g->stream)
+        if (cudaStreamCreateWithPriority(&s, cudaStreamNonBlocking, hi) != cudaSuccess) return undo(GR_ECUDA);
+    for (auto &ph : g->ph)
+        for (auto &e : ph.ev_out)
+            if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return undo(GR_ECUDA);
     return GR_OK;
 }
 
@@ -675,7 +932,10 @@ static int mark_common(gr_ctx *c, int32_t rank, int32_t t, void *dev_ptr) {
         c->h_ptr[t] = (uint64_t)(uintptr_t)dev_ptr;
         c->ptr_dirty = true;                            // re-upload only when it changed
     }
-    std::atomic_thread_fence(std::memory_order_release);
+    // the cycle's snapshot (step_impl, under mu) takes this bit together with the pointer
+    // table, so a tensor is seen by a cycle only if its pointer travels with that cycle
+    const int32_t b = c->bit_of[t];
+    c->h_marked[b >> 5] |= 1u << (b & 31);
     return GR_OK;
 }
 
@@ -686,7 +946,7 @@ int gr_mark_ready(gr_ctx *c, int32_t rank, int32_t t, void *dev_ptr) {
     if (rc) return rc;
     c->need_compute_fence = true;
     const int32_t b = c->bit_of[t];
-    __atomic_fetch_or(&c->h_bits[b >> 5], 1u << (b & 31), __ATOMIC_RELEASE);
+    c->h_bits[b >> 5] |= 1u << (b & 31);
     return GR_OK;
 }
 
@@ -710,7 +970,7 @@ int gr_mark_ready_batch(gr_ctx *c, int32_t rank, int32_t n, const int32_t *ids, 
         int rc = mark_common(c, rank, ids[i], ptrs[i]);
         if (rc) return rc;
         const int32_t b = c->bit_of[ids[i]];
-        __atomic_fetch_or(&c->h_bits[b >> 5], 1u << (b & 31), __ATOMIC_RELEASE);
+        c->h_bits[b >> 5] |= 1u << (b & 31);
     }
     if (n > 0) c->need_compute_fence = true;
     return GR_OK;
@@ -728,6 +988,8 @@ int gr_mark_ready_async(gr_ctx *c, int32_t rank, int32_t t, void *dev_ptr, void 
     CUresult r = c->write_value32((CUstream)stream, (CUdeviceptr)(c->d_flags + c->bit_of[t]), c->epoch, 0);
     if (r != CUDA_SUCCESS) {
         c->marked[t] = 0;
+        const int32_t b = c->bit_of[t];
+        c->h_marked[b >> 5] &= ~(1u << (b & 31));
         return fail(c, GR_ECUDA, "cuStreamWriteValue32 failed (%d)", (int)r);
     }
     return GR_OK;
@@ -771,9 +1033,20 @@ static int step_impl(gr_ctx *c, int32_t *released, gr_cycle_info *info, uint32_t
     }
     uint32_t epoch;
     int32_t abort_flag, shutdown_flag;
-    bool p_inline = false, step_fresh = false, async_used = false;
-    uint32_t inline_bits[GR_BV_INLINE_WORDS];
+    bool p_inline = c->W <= GR_BV_INLINE_WORDS, step_fresh = false, async_used = false;
+    gr::BvParams p{};
+    // the pointer-table snapshot buffer this cycle may use (its previous upload has long run)
+    const int pk = c->ptr_stage_next;
+    if (c->ptr_stage_pending[pk]) {
+        CK(c, cudaEventSynchronize(c->ev_ptr_stage[pk]));
+        c->ptr_stage_pending[pk] = false;
+    }
+    bool ptr_upload = false;
+    uint32_t *bits_stage = p_inline ? nullptr : c->h_bits_stage + (size_t)slot * 2 * c->W;
     {
+        // ONE critical section takes everything a concurrent gr_mark_ready could change: the
+        // compute-stream fence, the mark bits and the pointer table. A mark that lands after it
+        // belongs to the next cycle, consistently for the fence, the bits and the pointer.
         std::lock_guard<std::mutex> lk(c->mu);
         if (c->step_complete) return fail(c, GR_ESTATE, "step complete: call gr_wait first");
         if (c->need_compute_fence) {  // order the data stream after the marked gradients' producers
@@ -785,16 +1058,24 @@ static int step_impl(gr_ctx *c, int32_t *released, gr_cycle_info *info, uint32_t
         step_fresh = c->step_fresh;
         c->step_fresh = false;
         async_used = c->async_used;
-        if (c->W <= GR_BV_INLINE_WORDS) {  // snapshot the host mark bits into the launch itself
-            p_inline = true;
-            for (int w = 0; w < c->W; ++w) inline_bits[w] = __atomic_load_n(&c->h_bits[w], __ATOMIC_ACQUIRE);
+        if (p_inline) {  // the mark bits travel in the launch parameters
+            memcpy(p.inline_bits, c->h_bits, sizeof(uint32_t) * c->W);
+            memcpy(p.inline_marked, c->h_marked, sizeof(uint32_t) * c->W);
+        } else {         // ... or in this ring slot's pinned snapshot, DMA'd before the kernel
+            memcpy(bits_stage, c->h_bits, sizeof(uint32_t) * c->W);
+            memcpy(bits_stage + c->W, c->h_marked, sizeof(uint32_t) * c->W);
+        }
+        if (c->ptr_dirty) {
+            memcpy(c->h_ptr_stage + (size_t)pk * c->T, c->h_ptr, sizeof(uint64_t) * c->T);
+            c->ptr_dirty = false;
+            ptr_upload = true;
         }
         abort_flag = c->abort_flag;
         shutdown_flag = c->shutdown_flag;
     }
 
-    gr::BvParams p{};
     p.host_bits = c->d_hbits_dev;
+    p.marked_bits = c->d_hbits_dev + c->W;
     p.dev_flags = c->d_flags;
     p.new_step = step_fresh;
     p.check_async = async_used;
@@ -829,7 +1110,6 @@ static int step_impl(gr_ctx *c, int32_t *released, gr_cycle_info *info, uint32_t
     p.use_inline = p_inline;
     p.drain = drain ? 1 : 0;
     p.err = c->h_err;
-    if (p_inline) memcpy(p.inline_bits, inline_bits, sizeof(uint32_t) * c->W);
 
     std::pair<cudaEvent_t, cudaEvent_t> evb{};
     if (c->timing) {
@@ -850,10 +1130,15 @@ static int step_impl(gr_ctx *c, int32_t *released, gr_cycle_info *info, uint32_t
             CK(c, cudaStreamWaitEvent(c->s_coord, c->ev_drain, 0));
         }
     }
-    if (!p_inline)  // larger bitvectors: one DMA of the pinned mark bits, stream-ordered before the kernel
-        CK(c, cudaMemcpyAsync(c->d_hbits_dev, c->h_bits, sizeof(uint32_t) * c->W, cudaMemcpyHostToDevice, c->s_coord));
-    int lrc = gr::launch_bitvector(p, c->s_coord);
-    if (lrc) return fail(c, GR_ECUDA, "bitvector launch: %s", cudaGetErrorString((cudaError_t)lrc));
+    if (!p_inline)  // larger bitvectors: one DMA of the cycle's snapshot, stream-ordered before the kernel
+        CK(c, cudaMemcpyAsync(c->d_hbits_dev, bits_stage, sizeof(uint32_t) * 2 * c->W, cudaMemcpyHostToDevice,
+                              c->s_coord));
+    if (c->vg) {
+        RC(vg_launch(c, 0, c->s_coord, &p, nullptr));
+    } else {
+        int lrc = gr::launch_bitvector(p, c->s_coord);
+        if (lrc) return fail(c, GR_ECUDA, "bitvector launch: %s", cudaGetErrorString((cudaError_t)lrc));
+    }
     if (c->timing) {
         CK(c, cudaEventRecord(evb.second, c->s_coord));
         c->pending_bv_ev.push_back(evb);
@@ -928,9 +1213,12 @@ static int step_impl(gr_ctx *c, int32_t *released, gr_cycle_info *info, uint32_t
             evd = get_ev_pair(c);
             CK(c, cudaEventRecord(evd.first, c->s_data));
         }
-        if (c->ptr_dirty) {  // gradient pointers marked since the last upload
-            c->ptr_dirty = false;
-            CK(c, cudaMemcpyAsync(c->d_ptr, c->h_ptr, sizeof(uint64_t) * c->T, cudaMemcpyHostToDevice, c->s_data));
+        if (ptr_upload) {  // gradient pointers changed since the last upload: this cycle's snapshot
+            CK(c, cudaMemcpyAsync(c->d_ptr, c->h_ptr_stage + (size_t)pk * c->T, sizeof(uint64_t) * c->T,
+                                  cudaMemcpyHostToDevice, c->s_data));
+            CK(c, cudaEventRecord(c->ev_ptr_stage[pk], c->s_data));
+            c->ptr_stage_pending[pk] = true;
+            c->ptr_stage_next = (pk + 1) % kPtrStages;
         }
         if (d.trace) CK(c, cudaMemsetAsync(d.trace, 0, sizeof(uint64_t) * c->trace_slot_u64, c->s_data));
         if (c->stats_on) {
@@ -941,8 +1229,12 @@ static int step_impl(gr_ctx *c, int32_t *released, gr_cycle_info *info, uint32_t
                 CK(c, cudaMemsetAsync(c->d_nonfinite, 0, sizeof(int32_t), c->s_data));
             }
         }
-        lrc = gr::launch_data(d, local, c->buf_f16, ctas, c->s_data);
-        if (lrc) return fail(c, GR_ECUDA, "data launch: %s", cudaGetErrorString((cudaError_t)lrc));
+        if (c->vg) {
+            RC(vg_launch(c, 1, c->s_data, nullptr, &d));
+        } else {
+            int lrc = gr::launch_data(d, local, c->buf_f16, ctas, c->s_data);
+            if (lrc) return fail(c, GR_ECUDA, "data launch: %s", cudaGetErrorString((cudaError_t)lrc));
+        }
         if (c->timing) {
             CK(c, cudaEventRecord(evd.second, c->s_data));
             c->pending_data_ev.push_back(evd);
@@ -1050,7 +1342,9 @@ static int start_next_step(gr_ctx *c) {
         c->step++;
         c->stats.steps++;
         std::fill(c->marked.begin(), c->marked.end(), 0);
-        memset(c->h_bits, 0, sizeof(uint32_t) * (size_t)c->W);  // no bitvector kernel is in flight
+        // the live tables only: every cycle's kernel reads its own snapshot
+        memset(c->h_bits, 0, sizeof(uint32_t) * (size_t)c->W);
+        memset(c->h_marked, 0, sizeof(uint32_t) * (size_t)c->W);
         c->step_fresh = true;
         c->async_used = false;
         c->async_streams.clear();

@@ -100,9 +100,11 @@ def main():
 
     rank = int(os.environ["RANK"])
     N = int(os.environ["WORLD_SIZE"])
-    # more ranks than GPUs (the N=8 path on a 4-GPU box): ranks share devices round-robin; the
-    # processes then time-slice each GPU, which is slow but exercises every N-rank code path
-    local = int(os.environ.get("LOCAL_RANK", rank)) % max(1, torch.cuda.device_count())
+    # one process per GPU: never time-share a device between spinning ranks (Xid 109 risk on
+    # this pool); the N-rank path on fewer GPUs is tests/test_gpu_virtual.py's job
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    if local >= torch.cuda.device_count():
+        raise SystemExit(f"rank {rank}: LOCAL_RANK {local} but only {torch.cuda.device_count()} GPUs")
     torch.cuda.set_device(local)
     dist.init_process_group("gloo")
     ag = make_allgather(None)

@@ -145,3 +145,74 @@ def run_drain_case_on_rank(ctx, case, r, seed, device, buffer_f16: bool, drain_a
         gs = host_inputs(case.numel, case.N, seed, t, False, "uniform", idx)
         check_values(out[idx], gs, case.N, buffer_f16, False, where=f"rank {r} seed {seed} tensor {t} (drain)")
     return log, h.hexdigest()
+
+
+def run_ranks(N: int, fn, timeout: float = 600.0):
+    """Run fn(r) for r in 0..N-1 concurrently, one thread per virtual rank (gr_init_virtual:
+    the ranks' collective calls must overlap, as N processes' would). Re-raises the first
+    failure with its rank; returns the per-rank results."""
+    import threading
+    import traceback
+
+    res, errs = [None] * N, [None] * N
+
+    def body(r):
+        try:
+            res[r] = fn(r)
+        except BaseException as e:  # noqa: BLE001 — reported below with the rank
+            errs[r] = (e, traceback.format_exc())
+
+    ths = [threading.Thread(target=body, args=(r,), daemon=True) for r in range(N)]
+    for t in ths:
+        t.start()
+    for t in ths:
+        t.join(timeout)
+    if any(t.is_alive() for t in ths):
+        raise TimeoutError(f"virtual ranks still running after {timeout} s")
+    for r, e in enumerate(errs):
+        if e is not None:
+            raise AssertionError(f"virtual rank {r}: {e[0]!r}\n{e[1]}")
+    return res
+
+
+def run_virtual_case(case, seed, device, buffer_f16: bool, grad_f16=None, kind="uniform", max_cycles=None,
+                     exact: bool = True, async_streams=None, before_step=None, stats: bool = False,
+                     drain_after=None, **world_kw):
+    """One case on N = case.N virtual ranks of `device` (gr_init_virtual): every rank replays its
+    schedule through the C ABI in its own thread and is checked against the oracle exactly as a
+    process of a real N-GPU run is (run_case_on_rank / run_drain_case_on_rank); then the
+    replicas must be bitwise identical. Returns the per-rank contexts' stats and logs."""
+    from paper_1909_11150_b200 import GR_F16, GR_F32, virtual_world
+
+    N = case.N
+    ctxs = virtual_world(world_size=N, device=device.index or 0, numel=case.numel, group_of=case.group_of,
+                         grad_f16=grad_f16, buffer_dtype=GR_F16 if buffer_f16 else GR_F32, **world_kw)
+    try:
+        if stats:
+            for c in ctxs:
+                c.gr_enable_grad_stats(True)
+
+        def one(r):
+            s = async_streams[r] if async_streams else None
+            if drain_after is not None:
+                log, h = run_drain_case_on_rank(ctxs[r], case, r, seed, device, buffer_f16, drain_after,
+                                                async_stream=s)
+            else:
+                log, h = run_case_on_rank(ctxs[r], case, r, seed, device, buffer_f16, grad_f16, kind,
+                                          max_cycles=max_cycles, async_stream=s, exact=exact,
+                                          before_step=before_step[r] if before_step else None)
+            ss = check_grad_stats(ctxs[r], case, seed, buffer_f16, grad_f16, kind, exact=exact,
+                                  where=f"rank {r} seed {seed}") if stats else None
+            return log, h, ss, ctxs[r].stats(), ctxs[r].query_int(5)
+
+        out = run_ranks(N, one)
+        hs = [o[1] for o in out]
+        assert len(set(hs)) == 1, f"seed {seed}: outputs differ across virtual ranks"
+        if stats:
+            for o in out[1:]:  # fp64 atomics: equal up to summation order
+                for a, b in zip(out[0][2], o[2]):
+                    assert abs(a - b) <= 1e-12 * max(abs(a), abs(b)) + 1e-300, "statistics differ across ranks"
+        return out
+    finally:
+        for c in ctxs:
+            c.gr_finalize()

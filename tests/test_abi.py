@@ -148,6 +148,8 @@ def _rank_main(rank, port, mismatch, q):
         numel = [100, 200, 301]
     if mismatch == "queue" and rank == 1:
         comm_ctas = 32  # sets the fused kernel's default queue lags: must agree across ranks
+    if mismatch == "invalid" and rank == 1:
+        numel = [100, 0, 300]  # rejected locally on rank 1 only: rank 0 must not hang
     try:
         ctx = Context(rank=rank, world_size=2, device=-1, numel=numel, group_of=[0, 1, 1],
                       comm_ctas=comm_ctas, allgather=make_allgather(None))
@@ -158,11 +160,13 @@ def _rank_main(rank, port, mismatch, q):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("mismatch", [None, "table", "queue"])
+@pytest.mark.parametrize("mismatch", [None, "table", "queue", "invalid"])
 def test_gloo_world2_init_consistency(mismatch):
     """gr_init is collective: identical tables agree on the cache/layout;
-    any difference makes gr_init fail with GR_EMISMATCH on every rank."""
-    from paper_1909_11150_b200.binding import GR_EMISMATCH
+    any difference makes gr_init fail with GR_EMISMATCH on every rank. A rank
+    whose own arguments are rejected still joins the init gather, so every rank fails
+    (GR_EINVAL) instead of its peers blocking."""
+    from paper_1909_11150_b200.binding import GR_EINVAL, GR_EMISMATCH
     ctxm = mp.get_context("spawn")
     q = ctxm.Queue()
     port = _free_port()
@@ -172,7 +176,10 @@ def test_gloo_world2_init_consistency(mismatch):
     res = sorted([q.get(timeout=120) for _ in range(2)])
     for p in ps:
         p.join(60)
-    if mismatch:
+    if mismatch == "invalid":
+        assert all(r[1] == "err" and r[2] == GR_EINVAL for r in res), res
+        assert "rank 1" in res[0][3], res
+    elif mismatch:
         assert all(r[1] == "err" and r[2] == GR_EMISMATCH for r in res), res
     else:
         assert all(r[1] == "ok" for r in res), res
@@ -231,3 +238,14 @@ def test_fused_reduce_kernel_uses_tma_and_multimem():
     in-switch reduction (LDGMC = multimem.ld_reduce)."""
     sass = _cuobjdump("-sass", "-fun", "_ZN2gr11xfer_kernelI6__halfLb0EEEvNS_10DataParamsE")
     assert "UBLKCP" in sass and "SYNCS.ARRIVE.TRANS64" in sass and "LDGMC" in sass
+
+
+def test_virtual_world_needs_a_device():
+    """gr_init_virtual validates before touching CUDA: a dry device, world sizes outside
+    2..8 and bad tables fail with GR_EINVAL and leave no contexts."""
+    from paper_1909_11150_b200 import GrError, virtual_world
+    from paper_1909_11150_b200.binding import GR_EINVAL
+    for kw in (dict(world_size=2, device=-1), dict(world_size=1, device=0), dict(world_size=9, device=0)):
+        with pytest.raises(GrError) as e:
+            virtual_world(numel=[8, 8], group_of=[0, 1], **kw)
+        assert e.value.code == GR_EINVAL, kw
