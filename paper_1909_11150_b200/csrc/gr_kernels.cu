@@ -385,7 +385,9 @@ int launch_bitvector(const BvParams &p, void *stream) {
 }
 
 int launch_bitvector_virtual(const BvParamsV &pv, void *stream) {
-    const BvParams &p = pv.r[0];  // W and G are the same on every rank (one table)
+    int r0 = 0;  // W and G are the same on every rank (one table): take a present rank's
+    while (r0 < pv.N - 1 && ((pv.absent >> r0) & 1u)) ++r0;
+    const BvParams &p = pv.r[r0];
     const size_t smem = sizeof(uint32_t) * (3 * (size_t)p.W + ((size_t)p.G + 31) / 32);
     bitvector_attrs();
     if (p.W > GR_BV_INLINE_WORDS) bitvector_kernel_v<1024><<<pv.N, 1024, smem, (cudaStream_t)stream>>>(pv);
@@ -1319,7 +1321,9 @@ int launch_data(const DataParams &p, int local, int buffer_f16, int ctas, void *
 template <typename BT, bool STATS>
 static int launch_data_v_t(const DataParamsV &pv, cudaStream_t s) {
     xfer_attrs<BT, STATS>();
-    xfer_kernel_v<BT, STATS><<<pv.N * pv.per, XF_THREADS, (size_t)pv.r[0].nstages * pv.r[0].stage_bytes, s>>>(pv);
+    int r0 = 0;  // the stage ring is the same on every rank: take a present rank's
+    while (r0 < pv.N - 1 && ((pv.absent >> r0) & 1u)) ++r0;
+    xfer_kernel_v<BT, STATS><<<pv.N * pv.per, XF_THREADS, (size_t)pv.r[r0].nstages * pv.r[r0].stage_bytes, s>>>(pv);
     return (int)cudaGetLastError();
 }
 

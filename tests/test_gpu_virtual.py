@@ -21,7 +21,7 @@ from workloads.schedules import Case, random_mark_schedule, random_partition, re
 pytestmark = pytest.mark.gpu
 
 ONE_SHOT, TWO_SHOT = 1 << 62, 0  # one_shot_max_bytes forcing each algorithm
-NS = [2, 4, 8]
+NS = [2, 3, 4, 8]
 
 
 @pytest.fixture(scope="module")

@@ -108,3 +108,79 @@ def test_emulated_arithmetic_within_north_star_tolerance(orc, N):
         assert np.all(np.abs(e16 - ref) <= 2.0 ** -10 * N * maxg)
         # the derived bound (input RN + output RN) is N times tighter
         assert np.all(np.abs(e16 - ref) <= 2.0 ** -10 * maxg)
+
+
+# ---- hand-derived pins of emulate at N >= 3 and at the reading-R8 boundary -----------------
+
+def _golden_emulate_cases():
+    with open(os.path.join(HERE, "golden", "emulate_vectors.json")) as f:
+        return json.load(f)["cases"]
+
+
+def _f32(xs):
+    return np.array([float(x) for x in xs], dtype=np.float32)
+
+
+def _check_golden(emulate, case):
+    gs = [_f32(g) for g in case["g"]]
+    assert len(gs) == case["N"]
+    out = emulate(gs, case["buffer_f16"], case["grad_f16"])
+    want = _f32(case["expect"])
+    nan = np.isnan(want)
+    return bool(np.array_equal(np.isnan(out), nan) and
+                np.array_equal(out[~nan].view(np.uint32), want[~nan].view(np.uint32)))
+
+
+@pytest.mark.parametrize("case", _golden_emulate_cases(), ids=lambda c: c["id"])
+def test_emulate_hand_derived_goldens(orc, case):
+    """tests/golden/emulate_vectors.json: rank-order fp32 sums at N = 3 and 8, x fl32(1/N),
+    the per-rank fp16 pack, scaling before the fp16 store (R8), fp16 subnormals, IEEE specials,
+    cancellation — each value worked by hand from the arithmetic (bit-exact, sign of zero too)."""
+    assert _check_golden(orc.emulate, case), case["id"]
+
+
+# Each mutation is a plausible mistake in orc_emulate; the goldens above must catch every one
+# (so the oracle's value arithmetic is pinned by something other than itself).
+_MUTATIONS = {
+    "fp64_accumulation": [("float acc = 0.0f;", "double acc = 0.0;")],
+    "scale_after_fp16_store": [("float y = acc * inv_n;\n        if (buffer_f16) y = orc_round_f16(y);",
+                                "float y = acc;\n        if (buffer_f16) y = orc_round_f16(y);\n        y = y * inv_n;")],
+    "divide_by_n": [("float y = acc * inv_n;", "float y = acc / (float)N;")],
+    "no_pack_rounding": [("float x = buffer_f16 ? orc_round_f16(g[r][i]) : g[r][i];", "float x = g[r][i];")],
+    "reverse_rank_order": [("float x = buffer_f16 ? orc_round_f16(g[r][i]) : g[r][i];",
+                            "float x = buffer_f16 ? orc_round_f16(g[N - 1 - r][i]) : g[N - 1 - r][i];")],
+    "no_grad_cast": [("if (grad_f16) y = orc_round_f16(y);", "")],
+}
+
+
+@pytest.mark.parametrize("mutation", sorted(_MUTATIONS))
+def test_goldens_catch_mutated_emulate(tmp_path, mutation):
+    """Mutation check of the pins: orc_emulate rebuilt with one plausible mistake (fp64
+    accumulation, scaling after the fp16 store, division by N, no per-rank fp16 pack, reversed
+    rank order, no final gradient cast) fails at least one hand-derived golden."""
+    import ctypes
+    import subprocess
+    src = open(os.path.join(os.path.dirname(HERE), "oracle", "gr_oracle.c")).read()
+    for old, new in _MUTATIONS[mutation]:
+        assert src.count(old) == 1, f"mutation {mutation}: pattern not found once"
+        src = src.replace(old, new)
+    c = tmp_path / "mut.c"
+    c.write_text(src)
+    so = tmp_path / "libmut.so"
+    subprocess.run(["gcc", "-std=c11", "-O1", "-fno-fast-math", "-ffp-contract=off", "-shared", "-fPIC",
+                    "-I", os.path.join(os.path.dirname(HERE), "oracle"), str(c), "-o", str(so)], check=True)
+    L = ctypes.CDLL(str(so))
+    L.orc_emulate.argtypes = [ctypes.c_int32, ctypes.c_int64, ctypes.c_void_p, ctypes.c_int, ctypes.c_int,
+                              ctypes.c_void_p]
+    L.orc_emulate.restype = None
+
+    def emulate(gs, b16, g16):
+        arrs = [np.ascontiguousarray(g, dtype=np.float32) for g in gs]
+        ptrs = (ctypes.c_void_p * len(arrs))(*[a.ctypes.data for a in arrs])
+        out = np.zeros(arrs[0].size, dtype=np.float32)
+        L.orc_emulate(len(arrs), arrs[0].size, ctypes.cast(ptrs, ctypes.c_void_p), int(b16), int(g16),
+                      out.ctypes.data_as(ctypes.c_void_p))
+        return out
+
+    failed = [c["id"] for c in _golden_emulate_cases() if not _check_golden(emulate, c)]
+    assert failed, f"no golden catches the mutation {mutation}"
