@@ -486,3 +486,20 @@ def test_marks_racing_steps(gpu, T):
         for t in range(T):
             assert torch.equal(xs[t], want[t]), (step, t)
     ctx.gr_finalize()
+
+
+@pytest.mark.parametrize("buf16", [True, False])
+def test_numeric_edges_n1(gpu, buf16):
+    """Numeric edge cases element by element against the oracle (workloads.values kind "edge"):
+    values near fp16's maximum, fp16 subnormals, values below fp16's smallest subnormal (flushed
+    by the pack), +-Inf and NaN (propagated), fp32 and fp16 gradients; bit-exact (NaN payloads
+    aside) and within the north-star tolerance on the finite elements."""
+    from tests.parity_lib import run_case_on_rank
+    rng = np.random.default_rng(41)
+    T = 9
+    numel = rng.integers(1, 100000, size=T).astype(np.int64)
+    case = Case(1, numel, random_partition(T, 3, rng), random_mark_schedule(1, T, 41, 2), 41)
+    for gf in (None, [t % 2 == 0 for t in range(T)]):
+        ctx = _ctx(case, buf16, grad_f16=gf)
+        run_case_on_rank(ctx, case, 0, 41, gpu, buf16, grad_f16=gf, kind="edge")
+        ctx.gr_finalize()

@@ -73,6 +73,24 @@ def test_virtual_edge_both_algorithms(gpu, n):
         run_virtual_case(case, seed, gpu, True, kind="int", one_shot_max_bytes=TWO_SHOT)
 
 
+@pytest.mark.parametrize("n", [2, 3, 4])
+def test_virtual_numeric_edges(gpu, n):
+    """Numeric edge cases across ranks (kind "edge"): N-rank sums above fp16's range whose mean
+    is inside it (reading R8: x1/N before the fp16 store), fp16 subnormal inputs and outputs,
+    exact cancellation between ranks (+0), +-Inf / NaN propagation; both algorithms, both
+    buffer precisions, fp16 and fp32 gradients — bit-exact against oracle.emulate."""
+    from tests.parity_lib import run_virtual_case
+    rng = np.random.default_rng(50 + n)
+    T = 7
+    numel = rng.integers(1, 120000, size=T).astype(np.int64)
+    case = Case(n, numel, random_partition(T, 3, rng), random_mark_schedule(n, T, 50 + n, 2), 50 + n)
+    gf = [t % 3 == 0 for t in range(T)]
+    for buf16 in (True, False):
+        for osm in (TWO_SHOT, ONE_SHOT):
+            run_virtual_case(case, 50 + n, gpu, buf16, grad_f16=gf, kind="edge", one_shot_max_bytes=osm,
+                             chunk_elems=4096)
+
+
 @pytest.mark.parametrize("n", NS)
 def test_virtual_fcn220m_full_size(gpu, n):
     """The bench workload (225,115,137 elements, 68 tensors, 10 groups) at full size, per-rank
