@@ -328,13 +328,21 @@ def main():
                 "peak": hbm if hbm else 6650.0, "unit": "GB/s",
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs" if hbm else "B200_PROFILING.md fallback",
                 "kernel": f"local_kernel<{'half' if buf16 else 'float'}>", "algorithmic_bytes_per_launch": alg_bytes,
-                "kernel_ms": round(kern_ms, 4)}
+                "kernel_ms": round(kern_ms, 4),
+                # SURVEY.md §8(d) cfg2 counts pack (p_g+p_b) + unpack (p_b+p_g) through a materialised
+                # fusion buffer: 12 B/elem at fp16. At N=1 no peer reads the buffer, so the kernel
+                # fuses pack->x1/N->unpack in registers (8 B/elem, bit-identical): on the survey's
+                # count the same kernel would read above 1 of peak, i.e. the buffer is not moved.
+                "survey_cfg2_bytes_per_elem": 2 * (4 + pb),
+                "frac_on_survey_bytes": round(E * 2 * (4 + pb) / (kern_ms * 1e-3) / 1e9 / (hbm if hbm else 6650.0), 4)}
     else:
         alg_bytes = int(2 * (N - 1) / N * S)  # bytes that must cross NVLink per direction per rank
         roof = {"bound": "nvlink", "achieved": round(alg_bytes / (kern_ms * 1e-3) / 1e9, 1), "peak": 770.0,
                 "unit": "GB/s", "peak_source": "B200_PROFILING.md measured peer copy per direction (900 nominal)",
                 "kernel": f"xfer_kernel<{'half' if buf16 else 'float'}>:{ {2: 'ONESHOT', 3: 'TWOSHOT', 4: 'NVLS'}.get(algo) }",
-                "algorithmic_bytes_per_launch": alg_bytes, "kernel_ms": round(kern_ms, 4)}
+                "algorithmic_bytes_per_launch": alg_bytes, "kernel_ms": round(kern_ms, 4),
+                "peak_north_star": 900.0,
+                "frac_of_north_star_900": round(alg_bytes / (kern_ms * 1e-3) / 1e9 / 900.0, 4)}
     roof["frac"] = round(roof["achieved"] / roof["peak"], 4)
     roof["traffic"] = None
     try:

@@ -275,6 +275,8 @@ typedef struct {
     double host_step_us;        /* summed host wall time inside gr_step */
     double host_wait_us;        /* part of it spent waiting for the bitvector kernel's hand-off */
     double bitvector_device_us; /* summed %globaltimer span of the bitvector kernels (start->hand-off) */
+    int64_t data_launches_skipped; /* cycles whose data launch was skipped: no group was complete
+                                      on this rank, so none could be released on any rank */
 } gr_stats;
 
 int gr_query(gr_ctx *ctx, int32_t kind, void *out, size_t bytes);

@@ -11,7 +11,8 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libgr.so")
+# GR_LIB_PATH: load another build of the same ABI (A/B measurements of two library versions)
+LIB_PATH = os.environ.get("GR_LIB_PATH") or os.path.join(_HERE, "libgr.so")
 
 GR_OK, GR_EINVAL, GR_ESTATE, GR_EMISMATCH, GR_ECUDA, GR_ETIMEOUT, GR_EABORT, GR_ESHUTDOWN, GR_ENOMEM = \
     0, -1, -2, -3, -4, -5, -6, -7, -8
@@ -46,7 +47,7 @@ class GrStats(ctypes.Structure):
                 ("data_launches", ctypes.c_int64), ("released_elems", ctypes.c_int64),
                 ("data_kernel_ms", ctypes.c_double), ("bitvector_kernel_ms", ctypes.c_double),
                 ("host_step_us", ctypes.c_double), ("host_wait_us", ctypes.c_double),
-                ("bitvector_device_us", ctypes.c_double)]
+                ("bitvector_device_us", ctypes.c_double), ("data_launches_skipped", ctypes.c_int64)]
 
 
 class GrError(RuntimeError):

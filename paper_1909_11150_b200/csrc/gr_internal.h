@@ -24,17 +24,20 @@ struct Chunk {
     int32_t seg_begin, seg_end;
 };
 
-// Written by the bitvector kernel into pinned host-mapped memory; the host
-// polls `seq`. Followed in memory by A[W] (u32) and released[G] (i32).
-struct HostResult {
-    volatile uint64_t seq;
-    int32_t status;          // 0 ok, 1 abort, 2 shutdown, 3 timeout
-    int32_t n_released;
-    int32_t step_complete;
-    int32_t total_chunks;
-    int64_t released_elems;
-    uint64_t t_start, t_populated, t_anded, t_end;  // %globaltimer (ns) phase stamps
+// Hand-off of a cycle's result from the bitvector kernel to the host: pinned host-mapped
+// 64-bit LL words (tag << 32 | payload), tag = the cycle's sequence number (low 32 bits, never
+// 0). Every word validates itself, so the kernel writes them from many threads with plain
+// stores and no system-scope fence; the host spins until every word it needs carries the tag.
+enum HandWord {
+    HW_STATUS = 0,        // 0 ok, 1 abort, 2 shutdown, 3 timeout
+    HW_NREL = 1,          // released groups n
+    HW_COMPLETE = 2,      // step complete
+    HW_CHUNKS = 3,        // chunks of the released groups
+    HW_ELEMS = 4,         // released elements (lo, hi)
+    HW_STAMPS = 6,        // %globaltimer (ns): start, populated, ANDed, end (lo, hi each)
+    HW_A = 14,            // A[W], then released[n]
 };
+inline int hand_words(int W, int G) { return HW_A + W + G; }
 
 struct HostError {
     volatile int32_t code;   // 0 none, 3 timeout in the data kernel, 10 + status: a drain cycle failed
@@ -54,6 +57,15 @@ struct DevCycle {
     int32_t pad;
 };
 
+// Per-group constants the bitvector kernel needs (one 24-byte record per group, so one load
+// wave fetches them all; staged in shared memory when they fit, see BvParams::stage_groups).
+struct GroupInfo {
+    int32_t bit_begin, bit_end;  // the group's contiguous cache-bit range [begin, end)
+    int32_t nchunks;             // fusion-buffer chunks of the group
+    int32_t nsub;                // local-kernel sub-items of the group
+    int64_t elems;               // gradient elements of the group
+};
+
 struct BvParams {
     const uint32_t *host_bits;       // device copy [W] of the host mark bits (DMA'd before the launch);
                                      // unused when W <= GR_BV_INLINE_WORDS (passed in inline_bits)
@@ -64,11 +76,8 @@ struct BvParams {
     uint32_t *rel_words;             // device [W]: tensor bits released so far in this step
     int32_t new_step;                // 1 on the first cycle of a step (rel_words restart at 0)
     int32_t check_async;             // 1 if gr_mark_ready_async was used in this step
-    const int32_t *group_bit_begin;  // device [G]
-    const int32_t *group_bit_end;    // device [G]
-    const int32_t *group_nchunks;    // device [G]
-    const int32_t *group_nsub;       // device [G]: local-kernel sub-items of the group
-    const int64_t *group_elems;      // device [G]
+    const GroupInfo *groups;         // device [G]
+    int32_t stage_groups;            // 1: copy `groups` into shared memory at kernel start
     const int32_t *big_groups;       // device [n_big]: groups spanning > 8 bitvector words
     int32_t n_big;
     uint64_t *slot[GR_MAX_RANKS];    // every rank's LL bitvector slots [2][W] (own = local)
@@ -76,14 +85,14 @@ struct BvParams {
     int32_t *out_cum;                // device [G+1] (ring slot)
     DevCycle *out_info;              // device (ring slot)
     int32_t *out_subcum;             // device [G+1] (ring slot): prefix of group_nsub over the list
-    HostResult *result;              // host-mapped
+    uint64_t *hand;                  // host-mapped hand-off words (HandWord layout)
     int32_t T, G, W, nbits, rank, N;
     uint32_t epoch;                  // training-step epoch (>= 1)
     uint32_t tag;                    // cycle tag written into each LL word (!= 0)
     int32_t parity;                  // cycle & 1
     int32_t abort_flag, shutdown_flag;
     uint64_t timeout_ns;
-    uint64_t seq;
+    uint32_t htag;                   // hand-off tag of this cycle (!= 0)
     int32_t use_inline;
     int32_t drain;                   // gr_step_drain: wait on the device until every unreleased
                                      // tensor of this rank is ready, no host hand-off awaited

@@ -59,6 +59,10 @@ __device__ __forceinline__ void st_relaxed_sys64(uint64_t *p, uint64_t v) {
 __device__ __forceinline__ void st_relaxed_sys32(uint32_t *p, uint32_t v) {
     asm volatile("st.relaxed.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
+// one self-validating 64-bit hand-off word to pinned host memory (a single PCIe write)
+__device__ __forceinline__ void st_hand(uint64_t *p, uint64_t v) {
+    asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
 __device__ __forceinline__ void fence_sys() { asm volatile("fence.sc.sys;" ::: "memory"); }
 __device__ __forceinline__ void fence_acq_rel_sys() { asm volatile("fence.acq_rel.sys;" ::: "memory"); }
 
@@ -93,9 +97,18 @@ __device__ __forceinline__ void bitvector_body(const BvParams &p) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
     const uint64_t t_start = globaltimer();
     if (tid == 0) { s_timeout = 0; s_elems = 0ull; }
-    // released bits of this step (a new step starts from none)
+    // released bits of this step (a new step starts from none); the group records are fetched
+    // in the same load wave (no dependent global round trips later in the cycle)
     for (int w = tid; w < W; w += blockDim.x) sR[w] = p.new_step ? 0u : p.rel_words[w];
     for (int i = tid; i < Gw; i += blockDim.x) sC[i] = 0u;
+    const GroupInfo *gi = p.groups;
+    if (p.stage_groups) {
+        GroupInfo *sG = reinterpret_cast<GroupInfo *>(smem + ((3 * W + Gw + 1) & ~1));
+        const uint2 *src = reinterpret_cast<const uint2 *>(p.groups);
+        uint2 *dst = reinterpret_cast<uint2 *>(sG);
+        for (int i = tid; i < 3 * G; i += blockDim.x) dst[i] = src[i];
+        gi = sG;
+    }
     __syncthreads();
 
     // ---- step 1: populate from pending requests, publish ----
@@ -211,7 +224,7 @@ __device__ __forceinline__ void bitvector_body(const BvParams &p) {
     };
     if (status == ST_OK) {
         for (int g = tid; g < G; g += blockDim.x) {
-            const int b0 = p.group_bit_begin[g], b1 = p.group_bit_end[g];
+            const int b0 = gi[g].bit_begin, b1 = gi[g].bit_end;
             if (((b1 - 1) >> 5) - (b0 >> 5) + 1 > GR_SMALL_GROUP_WORDS) continue;
             bool ok = true;
             for (int w = b0 >> 5; ok && w <= ((b1 - 1) >> 5); ++w) {
@@ -222,7 +235,7 @@ __device__ __forceinline__ void bitvector_body(const BvParams &p) {
         }
         for (int i = warp; i < p.n_big; i += nwarps) {
             const int g = p.big_groups[i];
-            const int b0 = p.group_bit_begin[g], b1 = p.group_bit_end[g];
+            const int b0 = gi[g].bit_begin, b1 = gi[g].bit_end;
             bool ok = true;
             for (int w = (b0 >> 5) + lane; w <= ((b1 - 1) >> 5); w += 32) {
                 const uint32_t m = word_mask(w, b0, b1);
@@ -242,9 +255,9 @@ __device__ __forceinline__ void bitvector_body(const BvParams &p) {
         for (uint32_t m = sC[i]; m; m &= m - 1) {
             const int g = i * 32 + __ffs(m) - 1;
             ++my_cnt;
-            my_ch += p.group_nchunks[g];
-            my_sub += p.group_nsub[g];
-            my_el += p.group_elems[g];
+            my_ch += gi[g].nchunks;
+            my_sub += gi[g].nsub;
+            my_el += gi[g].elems;
         }
     int xc = my_cnt, xh = my_ch, xs = my_sub;  // inclusive warp scans
 #pragma unroll
@@ -275,7 +288,8 @@ __device__ __forceinline__ void bitvector_body(const BvParams &p) {
         s_tot[2] = s0;
     }
     __syncthreads();
-    int32_t *hrel = reinterpret_cast<int32_t *>(reinterpret_cast<uint32_t *>(p.result + 1) + W);
+    const uint64_t htg = (uint64_t)p.htag << 32;
+    uint64_t *hrel = p.hand + HW_A + W;  // released list, LL words
     {
         int idx = s_scan[warp][0] + xc - my_cnt, ch = s_scan[warp][1] + xh - my_ch;
         int sbase = s_scan[warp][2] + xs - my_sub;
@@ -285,11 +299,11 @@ __device__ __forceinline__ void bitvector_body(const BvParams &p) {
                 p.out_released[idx] = g;
                 p.out_cum[idx] = ch;
                 p.out_subcum[idx] = sbase;
-                hrel[idx] = g;
+                st_hand(hrel + idx, htg | (uint32_t)g);
                 ++idx;
-                ch += p.group_nchunks[g];
-                sbase += p.group_nsub[g];
-                const int b0 = p.group_bit_begin[g], b1 = p.group_bit_end[g];
+                ch += gi[g].nchunks;
+                sbase += gi[g].nsub;
+                const int b0 = gi[g].bit_begin, b1 = gi[g].bit_end;
                 for (int w = b0 >> 5; w <= ((b1 - 1) >> 5); ++w) atomicOr(&sR[w], word_mask(w, b0, b1));
             }
     }
@@ -311,27 +325,34 @@ __device__ __forceinline__ void bitvector_body(const BvParams &p) {
     const unsigned wall = __reduce_and_sync(0xffffffffu, all ? 1u : 0u);
     if (lane == 0) s_all[warp] = (int)wall;
 
-    // ---- hand the result over: device copy for the data kernel, pinned copy for the host ----
-    uint32_t *hA = reinterpret_cast<uint32_t *>(p.result + 1);
-    for (int w = tid; w < W; w += blockDim.x) hA[w] = sA[w];
+    // ---- hand the result over: device copy for the data kernel, LL words for the host (no
+    // fence: each word carries the cycle's tag, written in one wave by many threads) ----
+    for (int w = tid; w < W; w += blockDim.x) st_hand(p.hand + HW_A + w, htg | sA[w]);
     __syncthreads();
+    int complete = 1;
+    for (int i = 0; i < nwarps; ++i) complete &= s_all[i];
+    if (status != ST_OK) complete = 0;
+    if (tid < HW_A) {
+        const uint64_t t_end = globaltimer();
+        const uint64_t elems = (uint64_t)s_elems;
+        uint32_t v;
+        if (tid == HW_STATUS) v = (uint32_t)status;
+        else if (tid == HW_NREL) v = (uint32_t)run_base;
+        else if (tid == HW_COMPLETE) v = (uint32_t)complete;
+        else if (tid == HW_CHUNKS) v = (uint32_t)run_ch;
+        else if (tid < HW_STAMPS) v = (uint32_t)(elems >> (32 * (tid - HW_ELEMS)));
+        else {
+            const int k = tid - HW_STAMPS;
+            const uint64_t t = (k >> 1) == 0 ? t_start : (k >> 1) == 1 ? t_populated : (k >> 1) == 2 ? t_anded : t_end;
+            v = (uint32_t)(t >> (32 * (k & 1)));
+        }
+        st_hand(p.hand + tid, htg | v);
+    }
     if (tid == 0) {
-        int complete = 1;
-        for (int i = 0; i < nwarps; ++i) complete &= s_all[i];
         p.out_info->n_released = (status == ST_OK) ? run_base : 0;
         p.out_info->total_chunks = (status == ST_OK) ? run_ch : 0;
         p.out_info->total_subs = (status == ST_OK) ? s_tot[2] : 0;
         p.out_info->elems = (status == ST_OK) ? (int64_t)s_elems : 0;
-        p.result->status = status;
-        p.result->n_released = run_base;
-        p.result->step_complete = (status == ST_OK) ? complete : 0;
-        p.result->total_chunks = run_ch;
-        p.result->released_elems = (int64_t)s_elems;
-        p.result->t_start = t_start;
-        p.result->t_populated = t_populated;
-        p.result->t_anded = t_anded;
-        p.result->t_end = globaltimer();
-        asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(&p.result->seq), "l"(p.seq) : "memory");
         // a drain cycle is not awaited by the host: a failure (or a step left incomplete)
         // is reported through the error block checked by the next gr_step / gr_wait
         if (p.drain && (status != ST_OK || !complete)) {
@@ -376,8 +397,13 @@ static void bitvector_attrs() {
     }
 }
 
+static size_t bitvector_smem(const BvParams &p) {
+    const size_t words = (3 * (size_t)p.W + ((size_t)p.G + 31) / 32 + 1) & ~(size_t)1;
+    return sizeof(uint32_t) * words + (p.stage_groups ? sizeof(GroupInfo) * (size_t)p.G : 0);
+}
+
 int launch_bitvector(const BvParams &p, void *stream) {
-    const size_t smem = sizeof(uint32_t) * (3 * (size_t)p.W + ((size_t)p.G + 31) / 32);
+    const size_t smem = bitvector_smem(p);
     bitvector_attrs();
     if (p.W > GR_BV_INLINE_WORDS) bitvector_kernel<1024><<<1, 1024, smem, (cudaStream_t)stream>>>(p);
     else bitvector_kernel<BV_THREADS><<<1, BV_THREADS, smem, (cudaStream_t)stream>>>(p);
@@ -388,7 +414,7 @@ int launch_bitvector_virtual(const BvParamsV &pv, void *stream) {
     int r0 = 0;  // W and G are the same on every rank (one table): take a present rank's
     while (r0 < pv.N - 1 && ((pv.absent >> r0) & 1u)) ++r0;
     const BvParams &p = pv.r[r0];
-    const size_t smem = sizeof(uint32_t) * (3 * (size_t)p.W + ((size_t)p.G + 31) / 32);
+    const size_t smem = bitvector_smem(p);
     bitvector_attrs();
     if (p.W > GR_BV_INLINE_WORDS) bitvector_kernel_v<1024><<<pv.N, 1024, smem, (cudaStream_t)stream>>>(pv);
     else bitvector_kernel_v<BV_THREADS><<<pv.N, BV_THREADS, smem, (cudaStream_t)stream>>>(pv);
@@ -566,8 +592,14 @@ __device__ __forceinline__ float grad_load1(const char *g, int64_t idx, bool f16
 // NEXT-2 epilogue (LARS needs ||g||^2 per tensor, dynamic loss scaling needs a non-finite
 // flag): accumulate the squares of the values as stored in the gradient
 // tensor and note any Inf/NaN. Per thread in registers; one warp reduction + atomic per piece.
+// Per lane the squares are summed in fp32 over one piece (a tensor's overlap with one warp
+// sub-item of the N=1 kernel: at most 8 vectors of 8 per lane at the default 2048-element
+// sub-item; with one staged sub-tile of the xfer kernel: at most 3), all terms non-negative,
+// so the partial's relative error stays below (7 + 8) * 2^-24 ~ 9e-7 (typically ~1e-7); the
+// warp's partials are then added in fp64 and accumulated per tensor in fp64 (R19).
+// One fp32 register instead of an fp64 pair helps the HBM-bound N=1 kernel keep its occupancy.
 struct GradStat {
-    double ss = 0.0;
+    float ss = 0.f;
     unsigned nf = 0;
     __device__ __forceinline__ void add8(const float (&x)[8], bool f16) {
         float s = 0.f;
@@ -577,16 +609,16 @@ struct GradStat {
             s = fmaf(v, v, s);
             nf |= !isfinite(v);
         }
-        ss += (double)s;
+        ss += s;
     }
     __device__ __forceinline__ void add1(float x, bool f16) {
         const float v = f16 ? __half2float(__float2half_rn(x)) : x;
-        ss += (double)v * (double)v;
+        ss = fmaf(v, v, ss);
         nf |= !isfinite(v);
     }
     // warp-collective: every lane of the warp must call it
     __device__ __forceinline__ void flush(double *sumsq, int32_t *nonfinite, int tensor) {
-        double v = ss;
+        double v = (double)ss;
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
         const unsigned anynf = __reduce_or_sync(0xffffffffu, nf);
@@ -594,7 +626,7 @@ struct GradStat {
             if (v != 0.0) atomicAdd(sumsq + tensor, v);
             if (anynf) atomicOr(nonfinite, 1);
         }
-        ss = 0.0;
+        ss = 0.f;
         nf = 0;
     }
 };
@@ -623,10 +655,17 @@ __device__ __forceinline__ int chunk_of_item(const DataParams &p, int nrel, int 
 constexpr int LC_THREADS = 256;
 // warp sub-items: p.lc_sub elements each, p.lc_subs slots per chunk
 constexpr int LC_UNROLL = 2;
+#ifndef GR_LC_STATS_UNROLL
+#define GR_LC_STATS_UNROLL 1  // STATS: one 32-B vector per lane in flight, no spills at 64 registers (measured 1.03x of the plain pass vs 1.09x with two)
+#endif
+#ifndef GR_LC_MINB
+#define GR_LC_MINB 4
+#endif
 
 template <typename BT, bool STATS>
-__global__ void __launch_bounds__(LC_THREADS, 3) local_kernel(const __grid_constant__ DataParams p) {
+__global__ void __launch_bounds__(LC_THREADS, GR_LC_MINB) local_kernel(const __grid_constant__ DataParams p) {
     using B = Buf<BT>;
+    constexpr int LCU = STATS ? GR_LC_STATS_UNROLL : LC_UNROLL;
     const int lane = threadIdx.x & 31;
     const int gw = blockIdx.x * (LC_THREADS / 32) + (threadIdx.x >> 5);
     const int nw = gridDim.x * (LC_THREADS / 32);
@@ -660,13 +699,13 @@ __global__ void __launch_bounds__(LC_THREADS, 3) local_kernel(const __grid_const
             const bool aligned = ((reinterpret_cast<uintptr_t>(g) + toff * (f16 ? 2 : 4)) & 15) == 0;
             const int64_t n = hi - lo;
             const int64_t nvec = aligned ? (n >> 3) : 0;
-            for (int64_t v0 = lane; v0 < nvec; v0 += 32 * LC_UNROLL) {
-                GradRaw gr[LC_UNROLL];
+            for (int64_t v0 = lane; v0 < nvec; v0 += 32 * LCU) {
+                GradRaw gr[LCU];
 #pragma unroll
-                for (int u = 0; u < LC_UNROLL; ++u)
+                for (int u = 0; u < LCU; ++u)
                     if (v0 + 32 * u < nvec) gr[u] = grad_load(g, toff + 8 * (v0 + 32 * u), f16);
 #pragma unroll
-                for (int u = 0; u < LC_UNROLL; ++u) {
+                for (int u = 0; u < LCU; ++u) {
                     const int64_t v = v0 + 32 * u;
                     if (v >= nvec) continue;
                     float x[8];

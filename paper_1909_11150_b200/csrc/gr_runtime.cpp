@@ -125,9 +125,10 @@ struct gr_ctx {
     Seg *d_segs = nullptr;
     Chunk *d_chunks = nullptr;
     int64_t *d_cbeg = nullptr, *d_cend = nullptr;
-    int32_t *d_gbb = nullptr, *d_gbe = nullptr, *d_gnch = nullptr, *d_gcb = nullptr, *d_gnsub = nullptr,
+    gr::GroupInfo *d_groups = nullptr;
+    bool stage_groups = false;  // the group records fit the bitvector kernel's shared memory
+    int32_t *d_gcb = nullptr,
             *d_gspc = nullptr, *d_subcum_ring = nullptr;
-    int64_t *d_gel = nullptr;
     int32_t *d_big = nullptr;
     uint32_t *d_relw = nullptr, *d_hbits_dev = nullptr;
     uint64_t *d_ptr = nullptr;
@@ -148,12 +149,12 @@ struct gr_ctx {
     cudaEvent_t ev_ptr_stage[kPtrStages] = {};
     bool ptr_stage_pending[kPtrStages] = {};
     int ptr_stage_next = 0;
-    gr::HostResult *h_res = nullptr;
+    uint64_t *h_hand = nullptr;   // hand-off words written by the bitvector kernel (HandWord)
     gr::HostError *h_err = nullptr;
     uint32_t *d_hbits = nullptr;
-    gr::HostResult *d_res = nullptr;
+    uint64_t *d_hand = nullptr;
     gr::HostError *d_err = nullptr;
-    size_t res_bytes = 0;
+    size_t hand_bytes = 0;
     PFN_writeValue32 write_value32 = nullptr;
     int data_ctas[4] = {0, 0, 0, 0};       // world.comm_ctas (or every SM)
     int data_ctas_full[4] = {0, 0, 0, 0};  // every SM (drain cycles)
@@ -165,6 +166,12 @@ struct gr_ctx {
     // step / cycle state
     std::mutex mu;
     std::vector<uint8_t> marked;
+    // locally complete groups: a group can be released globally only if every rank marked all
+    // its tensors, so when no unreleased group is complete HERE, nothing can be released in
+    // this cycle on ANY rank and the data launch is skipped (its kernel would exit at once)
+    std::vector<int32_t> grp_size, grp_marked;
+    std::vector<uint8_t> grp_released;
+    int32_t n_ready_groups = 0;
     uint32_t epoch = 1;
     int64_t cycle = 0, step = 0;
     uint64_t seq = 0;
@@ -194,7 +201,7 @@ struct gr_ctx {
     struct TraceCycle {
         int64_t cycle, step;
         uint64_t k_start, k_pop, k_and, k_end;
-        int64_t h_enter_ns, h_launched_ns, h_seen_ns, h_done_ns;
+        int64_t h_enter_ns, h_snap_ns, h_bv_ns, h_launched_ns, h_seen_ns, h_done_ns;
         int n_released, algo, nitems, slot;
         int64_t elems;
     };
@@ -283,11 +290,14 @@ int build_layouts(gr_ctx *c, const gr_tensor *table, const int32_t *group_of) {
     c->nbits = GR_STATUS_BITS + T;
     c->W = (c->nbits + 31) / 32;
     {   // the bitvector kernel keeps L, A, released words and the complete-group mask in shared
-        // memory (64 KB opt-in): about 131,000 tensors at most
-        const size_t smem = sizeof(uint32_t) * (3 * (size_t)c->W + ((size_t)G + 31) / 32);
+        // memory (64 KB opt-in): about 131,000 tensors at most; the 24-byte group records join
+        // them when they fit (up to 1,024 groups)
+        const size_t words = (3 * (size_t)c->W + ((size_t)G + 31) / 32 + 1) & ~(size_t)1;
+        const size_t smem = sizeof(uint32_t) * words;
         if (smem > 64 * 1024)
             return fail(nullptr, GR_EINVAL, "%d tensors / %d groups exceed the bitvector kernel's 64 KB "
                         "shared-memory budget (%zu B)", T, G, smem);
+        c->stage_groups = G <= 1024 && smem + sizeof(gr::GroupInfo) * (size_t)G <= 64 * 1024;
     }
     c->bit_of.assign(T, 0);
     c->tensor_of_bit.assign((size_t)c->W * 32, -1);
@@ -473,13 +483,14 @@ int setup_local(gr_ctx *c) {
     RC(upload(c, &c->d_chunks, c->chunks));
     RC(upload(c, &c->d_cbeg, c->chunk_begin));
     RC(upload(c, &c->d_cend, c->chunk_end));
-    RC(upload(c, &c->d_gbb, c->gbit_begin));
-    RC(upload(c, &c->d_gbe, c->gbit_end));
-    RC(upload(c, &c->d_gnch, c->gnchunks));
+    {
+        std::vector<gr::GroupInfo> gi(c->G);
+        for (int32_t g = 0; g < c->G; ++g)
+            gi[g] = gr::GroupInfo{c->gbit_begin[g], c->gbit_end[g], c->gnchunks[g], c->gnsub[g], c->gelems[g]};
+        RC(upload(c, &c->d_groups, gi));
+    }
     RC(upload(c, &c->d_gcb, c->gchunk_begin));
-    RC(upload(c, &c->d_gnsub, c->gnsub));
     RC(upload(c, &c->d_gspc, c->gspc));
-    RC(upload(c, &c->d_gel, c->gelems));
     RC(upload(c, &c->d_big, c->big_groups));
     CK(c, cudaMalloc((void **)&c->d_relw, sizeof(uint32_t) * c->W));
     CK(c, cudaMemset(c->d_relw, 0, sizeof(uint32_t) * c->W));
@@ -507,13 +518,13 @@ int setup_local(gr_ctx *c) {
     CK(c, cudaHostAlloc((void **)&c->h_ptr_stage, sizeof(uint64_t) * c->T * kPtrStages, hf));
     if (c->W > GR_BV_INLINE_WORDS)
         CK(c, cudaHostAlloc((void **)&c->h_bits_stage, sizeof(uint32_t) * 2 * (size_t)c->W * GR_SLOT_RING, hf));
-    c->res_bytes = sizeof(gr::HostResult) + sizeof(uint32_t) * c->W + sizeof(int32_t) * c->G;
-    CK(c, cudaHostAlloc((void **)&c->h_res, c->res_bytes, hf));
-    memset((void *)c->h_res, 0, c->res_bytes);
+    c->hand_bytes = sizeof(uint64_t) * gr::hand_words(c->W, c->G);
+    CK(c, cudaHostAlloc((void **)&c->h_hand, c->hand_bytes, hf));
+    memset((void *)c->h_hand, 0, c->hand_bytes);  // tag 0: never a cycle's tag
     CK(c, cudaHostAlloc((void **)&c->h_err, sizeof(gr::HostError), hf));
     memset((void *)c->h_err, 0, sizeof(gr::HostError));
     CK(c, cudaHostGetDevicePointer((void **)&c->d_hbits, c->h_bits, 0));
-    CK(c, cudaHostGetDevicePointer((void **)&c->d_res, (void *)c->h_res, 0));
+    CK(c, cudaHostGetDevicePointer((void **)&c->d_hand, (void *)c->h_hand, 0));
     CK(c, cudaHostGetDevicePointer((void **)&c->d_err, (void *)c->h_err, 0));
 
     // stream memory operations for gr_mark_ready_async
@@ -623,8 +634,8 @@ void free_all(gr_ctx *c) {
         if (!c->vg && r != c->rank && c->peer_symm[r]) cudaIpcCloseMemHandle(c->peer_symm[r]);
     gr::nvls_free(c->nvls);
     cudaFree(c->symm);
-    void *dptrs[] = {c->d_segs, c->d_chunks, c->d_cbeg, c->d_cend, c->d_gbb, c->d_gbe, c->d_gnch, c->d_gcb,
-                     c->d_gel, c->d_big, c->d_relw, c->d_hbits_dev, c->d_ptr, c->d_rel_ring, c->d_cum_ring, c->d_info_ring, c->d_counters, c->d_gnsub, c->d_gspc, c->d_subcum_ring,
+    void *dptrs[] = {c->d_segs, c->d_chunks, c->d_cbeg, c->d_cend, c->d_groups, c->d_gcb,
+                     c->d_big, c->d_relw, c->d_hbits_dev, c->d_ptr, c->d_rel_ring, c->d_cum_ring, c->d_info_ring, c->d_counters, c->d_gspc, c->d_subcum_ring,
                      c->d_flags, c->d_trace, c->d_sumsq, c->d_nonfinite};
     for (void *p : dptrs) cudaFree(p);
     cudaFreeHost(c->h_bits);
@@ -636,7 +647,7 @@ void free_all(gr_ctx *c) {
         if (c->ev_ptr_stage[i]) cudaEventDestroy(c->ev_ptr_stage[i]);
     for (int i = 0; i < 2; ++i)
         if (c->ev_vin[i]) cudaEventDestroy(c->ev_vin[i]);
-    cudaFreeHost((void *)c->h_res);
+    cudaFreeHost((void *)c->h_hand);
     cudaFreeHost((void *)c->h_err);
     for (int i = 0; i < GR_SLOT_RING; ++i)
         if (c->ring_ev[i]) cudaEventDestroy(c->ring_ev[i]);
@@ -814,6 +825,10 @@ static int create_ctx(gr_ctx **out, const gr_world *world, const gr_tensor *tabl
         return rc;
     }
     c->marked.assign(T, 0);
+    c->grp_size.assign(G, 0);
+    for (int32_t t = 0; t < T; ++t) c->grp_size[group_of[t]]++;
+    c->grp_marked.assign(G, 0);
+    c->grp_released.assign(G, 0);
     c->dev = c->dry ? -1 : world->device;
     *out = c;
     return GR_OK;
@@ -928,6 +943,7 @@ static int mark_common(gr_ctx *c, int32_t rank, int32_t t, void *dev_ptr) {
     if (c->step_complete) return fail(c, GR_ESTATE, "step complete: call gr_wait before marking again");
     if (c->marked[t]) return fail(c, GR_ESTATE, "tensor %d already marked in this step", t);
     c->marked[t] = 1;
+    if (++c->grp_marked[c->group_of[t]] == c->grp_size[c->group_of[t]]) c->n_ready_groups++;
     if (c->h_ptr[t] != (uint64_t)(uintptr_t)dev_ptr) {  // pointer first, then the flag
         c->h_ptr[t] = (uint64_t)(uintptr_t)dev_ptr;
         c->ptr_dirty = true;                            // re-upload only when it changed
@@ -988,6 +1004,7 @@ int gr_mark_ready_async(gr_ctx *c, int32_t rank, int32_t t, void *dev_ptr, void 
     CUresult r = c->write_value32((CUstream)stream, (CUdeviceptr)(c->d_flags + c->bit_of[t]), c->epoch, 0);
     if (r != CUDA_SUCCESS) {
         c->marked[t] = 0;
+        if (c->grp_marked[c->group_of[t]]-- == c->grp_size[c->group_of[t]]) c->n_ready_groups--;
         const int32_t b = c->bit_of[t];
         c->h_marked[b >> 5] &= ~(1u << (b & 31));
         return fail(c, GR_ECUDA, "cuStreamWriteValue32 failed (%d)", (int)r);
@@ -1041,7 +1058,7 @@ static int step_impl(gr_ctx *c, int32_t *released, gr_cycle_info *info, uint32_t
         CK(c, cudaEventSynchronize(c->ev_ptr_stage[pk]));
         c->ptr_stage_pending[pk] = false;
     }
-    bool ptr_upload = false;
+    bool ptr_upload = false, skip_data = false;
     uint32_t *bits_stage = p_inline ? nullptr : c->h_bits_stage + (size_t)slot * 2 * c->W;
     {
         // ONE critical section takes everything a concurrent gr_mark_ready could change: the
@@ -1049,7 +1066,9 @@ static int step_impl(gr_ctx *c, int32_t *released, gr_cycle_info *info, uint32_t
         // belongs to the next cycle, consistently for the fence, the bits and the pointer.
         std::lock_guard<std::mutex> lk(c->mu);
         if (c->step_complete) return fail(c, GR_ESTATE, "step complete: call gr_wait first");
-        if (c->need_compute_fence) {  // order the data stream after the marked gradients' producers
+        // virtual ranks fire one data launch over all ranks, so they never skip it
+        skip_data = !drain && !c->vg && c->n_ready_groups == 0;
+        if (c->need_compute_fence && !skip_data) {  // order the data stream after the marked gradients' producers
             CK(c, cudaEventRecord(c->ev_compute, c->s_compute));
             CK(c, cudaStreamWaitEvent(c->s_data, c->ev_compute, 0));
             c->need_compute_fence = false;
@@ -1065,7 +1084,7 @@ static int step_impl(gr_ctx *c, int32_t *released, gr_cycle_info *info, uint32_t
             memcpy(bits_stage, c->h_bits, sizeof(uint32_t) * c->W);
             memcpy(bits_stage + c->W, c->h_marked, sizeof(uint32_t) * c->W);
         }
-        if (c->ptr_dirty) {
+        if (c->ptr_dirty && !skip_data) {
             memcpy(c->h_ptr_stage + (size_t)pk * c->T, c->h_ptr, sizeof(uint64_t) * c->T);
             c->ptr_dirty = false;
             ptr_upload = true;
@@ -1074,16 +1093,14 @@ static int step_impl(gr_ctx *c, int32_t *released, gr_cycle_info *info, uint32_t
         shutdown_flag = c->shutdown_flag;
     }
 
+    const auto h_snap = std::chrono::steady_clock::now();
     p.host_bits = c->d_hbits_dev;
     p.marked_bits = c->d_hbits_dev + c->W;
     p.dev_flags = c->d_flags;
     p.new_step = step_fresh;
     p.check_async = async_used;
-    p.group_bit_begin = c->d_gbb;
-    p.group_bit_end = c->d_gbe;
-    p.group_nchunks = c->d_gnch;
-    p.group_nsub = c->d_gnsub;
-    p.group_elems = c->d_gel;
+    p.groups = c->d_groups;
+    p.stage_groups = c->stage_groups ? 1 : 0;
     p.big_groups = c->d_big;
     p.n_big = (int32_t)c->big_groups.size();
     p.rel_words = c->d_relw;
@@ -1092,7 +1109,7 @@ static int step_impl(gr_ctx *c, int32_t *released, gr_cycle_info *info, uint32_t
     p.out_cum = c->d_cum_ring + (size_t)slot * (c->G + 1);
     p.out_info = c->d_info_ring + slot;
     p.out_subcum = c->d_subcum_ring + (size_t)slot * (c->G + 1);
-    p.result = c->d_res;
+    p.hand = c->d_hand;
     p.T = c->T;
     p.G = c->G;
     p.W = c->W;
@@ -1106,7 +1123,8 @@ static int step_impl(gr_ctx *c, int32_t *released, gr_cycle_info *info, uint32_t
     p.abort_flag = abort_flag;
     p.shutdown_flag = shutdown_flag;
     p.timeout_ns = (uint64_t)c->world.timeout_ms * 1000000ull;
-    p.seq = ++c->seq;
+    if ((uint32_t)++c->seq == 0) ++c->seq;  // the hand-off tag is the low 32 bits, never 0
+    p.htag = (uint32_t)c->seq;
     p.use_inline = p_inline;
     p.drain = drain ? 1 : 0;
     p.err = c->h_err;
@@ -1144,11 +1162,15 @@ static int step_impl(gr_ctx *c, int32_t *released, gr_cycle_info *info, uint32_t
         c->pending_bv_ev.push_back(evb);
     }
     c->stats.bitvector_launches++;
+    const auto h_bv = std::chrono::steady_clock::now();
 
     // Data kernel, launched now (before the host sees the cycle's result): it waits on the
     // bitvector kernel through an event and reads the released set from device memory, so
-    // the reduction starts the moment the bitvector kernel ends. Empty cycles exit at once.
-    {
+    // the reduction starts the moment the bitvector kernel ends. Empty cycles exit at once;
+    // cycles that cannot release anything (no locally complete group) do not launch it.
+    if (skip_data) {
+        c->stats.data_launches_skipped++;
+    } else {
         gr::DataParams d{};
         d.segs = c->d_segs;
         d.chunks = c->d_chunks;
@@ -1252,12 +1274,21 @@ static int step_impl(gr_ctx *c, int32_t *released, gr_cycle_info *info, uint32_t
         return GR_OK;
     }
 
-    // wait for the kernel's hand-off (pinned host memory), bounded
+    // wait for the kernel's hand-off (pinned host memory, LL words tagged with this cycle), bounded
     const auto t0 = std::chrono::steady_clock::now();
     const auto h_launched = t0;
     const auto limit = std::chrono::milliseconds(c->world.timeout_ms + 5000);
+    const uint64_t *H = c->h_hand;
+    auto word_ready = [&](int i) { return (uint32_t)(__atomic_load_n(H + i, __ATOMIC_ACQUIRE) >> 32) == p.htag; };
+    auto word = [&](int i) { return (uint32_t)__atomic_load_n(H + i, __ATOMIC_RELAXED); };
     uint64_t spins = 0;
-    while (c->h_res->seq != p.seq) {
+    int need = gr::HW_A + c->W;  // header + A; then the released list once n is known
+    for (int i = 0; i < need;) {
+        if (word_ready(i)) {
+            if (i == gr::HW_NREL) need += (int)std::min<uint32_t>(word(gr::HW_NREL), (uint32_t)c->G);
+            ++i;
+            continue;
+        }
         if ((++spins & 1023) == 0) {
             cudaError_t q = cudaStreamQuery(c->s_coord);
             if (q != cudaSuccess && q != cudaErrorNotReady)
@@ -1267,23 +1298,34 @@ static int step_impl(gr_ctx *c, int32_t *released, gr_cycle_info *info, uint32_t
             if (spins > (1u << 20)) std::this_thread::yield();
         }
     }
-    std::atomic_thread_fence(std::memory_order_acquire);
     const auto h_seen = std::chrono::steady_clock::now();
+    auto word64 = [&](int i) { return (uint64_t)word(i) | ((uint64_t)word(i + 1) << 32); };
+    const uint64_t k_start = word64(gr::HW_STAMPS), k_pop = word64(gr::HW_STAMPS + 2),
+                   k_and = word64(gr::HW_STAMPS + 4), k_end = word64(gr::HW_STAMPS + 6);
     c->stats.host_wait_us += std::chrono::duration<double, std::micro>(h_seen - t0).count();
-    c->stats.bitvector_device_us += (double)(c->h_res->t_end - c->h_res->t_start) * 1e-3;
-    const int status = c->h_res->status;
-    const uint32_t *hA = reinterpret_cast<const uint32_t *>(c->h_res + 1);
-    const int32_t *hrel = reinterpret_cast<const int32_t *>(hA + c->W);
-    if (global_bits) memcpy(global_bits, hA, sizeof(uint32_t) * c->W);
+    c->stats.bitvector_device_us += (double)(k_end - k_start) * 1e-3;
+    const int status = (int)word(gr::HW_STATUS);
+    if (global_bits)
+        for (int w = 0; w < c->W; ++w) global_bits[w] = word(gr::HW_A + w);
     const int64_t this_cycle = c->cycle++;
     c->stats.cycles++;
     if (status == gr::ST_TIMEOUT) return fail(c, GR_ETIMEOUT, "cycle %lld: a peer did not publish its bitvector", (long long)this_cycle);
     if (status == gr::ST_ABORT) return fail(c, GR_EABORT, "cycle %lld: a rank raised ABORT", (long long)this_cycle);
     if (status == gr::ST_SHUTDOWN) return fail(c, GR_ESHUTDOWN, "cycle %lld: a rank raised SHUTDOWN", (long long)this_cycle);
-    const int n = c->h_res->n_released;
-    const int total_chunks = c->h_res->total_chunks;
-    const int64_t rel_elems = c->h_res->released_elems;
-    memcpy(released, hrel, sizeof(int32_t) * n);
+    const int n = (int)word(gr::HW_NREL);
+    const int total_chunks = (int)word(gr::HW_CHUNKS);
+    const int64_t rel_elems = (int64_t)word64(gr::HW_ELEMS);
+    for (int i = 0; i < n; ++i) released[i] = (int32_t)word(gr::HW_A + c->W + i);
+    if (n > 0) {
+        std::lock_guard<std::mutex> lk(c->mu);
+        for (int i = 0; i < n; ++i) {
+            const int32_t g = released[i];
+            if (g >= 0 && g < c->G && !c->grp_released[g]) {
+                c->grp_released[g] = 1;
+                c->n_ready_groups--;  // released groups were complete on every rank, this one too
+            }
+        }
+    }
 
     if (n > 0) {
         const int64_t msg_bytes = rel_elems * (c->buf_f16 ? 2 : 4);
@@ -1293,7 +1335,7 @@ static int step_impl(gr_ctx *c, int32_t *released, gr_cycle_info *info, uint32_t
                                         : (c->nvls.enabled ? gr::ALGO_NVLS : gr::ALGO_TWOSHOT));
         c->stats.released_elems += rel_elems;
     }
-    const int complete = c->h_res->step_complete;
+    const int complete = (int)word(gr::HW_COMPLETE);
     const auto h_done = std::chrono::steady_clock::now();
     c->stats.host_step_us += std::chrono::duration<double, std::micro>(h_done - h_enter).count();
     if (!c->trace_path.empty() && c->trace_written < c->trace_max) {
@@ -1304,11 +1346,13 @@ static int step_impl(gr_ctx *c, int32_t *released, gr_cycle_info *info, uint32_t
         gr_ctx::TraceCycle tc{};
         tc.cycle = this_cycle;
         tc.step = c->step;
-        tc.k_start = c->h_res->t_start;
-        tc.k_pop = c->h_res->t_populated;
-        tc.k_and = c->h_res->t_anded;
-        tc.k_end = c->h_res->t_end;
+        tc.k_start = k_start;
+        tc.k_pop = k_pop;
+        tc.k_and = k_and;
+        tc.k_end = k_end;
         tc.h_enter_ns = ns(h_enter);
+        tc.h_snap_ns = ns(h_snap);
+        tc.h_bv_ns = ns(h_bv);
         tc.h_launched_ns = ns(h_launched);
         tc.h_seen_ns = ns(h_seen);
         tc.h_done_ns = ns(h_done);
@@ -1342,6 +1386,9 @@ static int start_next_step(gr_ctx *c) {
         c->step++;
         c->stats.steps++;
         std::fill(c->marked.begin(), c->marked.end(), 0);
+        std::fill(c->grp_marked.begin(), c->grp_marked.end(), 0);
+        std::fill(c->grp_released.begin(), c->grp_released.end(), 0);
+        c->n_ready_groups = 0;
         // the live tables only: every cycle's kernel reads its own snapshot
         memset(c->h_bits, 0, sizeof(uint32_t) * (size_t)c->W);
         memset(c->h_marked, 0, sizeof(uint32_t) * (size_t)c->W);
@@ -1396,7 +1443,8 @@ int gr_wait(gr_ctx *c) {
         for (const auto &tc : c->trace_cycles) {
             f << "{\"cycle\":" << tc.cycle << ",\"step\":" << tc.step << ",\"rank\":" << c->rank
               << ",\"N\":" << c->N << ",\"k\":[" << tc.k_start << "," << tc.k_pop << "," << tc.k_and << ","
-              << tc.k_end << "],\"h\":[" << tc.h_enter_ns << "," << tc.h_launched_ns << "," << tc.h_seen_ns
+              << tc.k_end << "],\"h\":[" << tc.h_enter_ns << "," << tc.h_snap_ns << "," << tc.h_bv_ns << ","
+              << tc.h_launched_ns << "," << tc.h_seen_ns
               << "," << tc.h_done_ns << "],\"n_released\":" << tc.n_released << ",\"algo\":" << tc.algo
               << ",\"elems\":" << tc.elems << ",\"nitems\":" << tc.nitems << ",\"items\":[";
             if (tc.nitems > 0) {

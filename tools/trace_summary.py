@@ -26,13 +26,16 @@ def main():
         kpop = [(r["k"][1] - r["k"][0]) / 1e3 for r in recs]
         kand = [(r["k"][2] - r["k"][1]) / 1e3 for r in recs]
         krel = [(r["k"][3] - r["k"][2]) / 1e3 for r in recs]
-        hl = [(r["h"][1] - r["h"][0]) / 1e3 for r in recs]
-        hw = [(r["h"][2] - r["h"][1]) / 1e3 for r in recs]
-        hd = [(r["h"][3] - r["h"][2]) / 1e3 for r in recs]
+        h = [r["h"] for r in recs]  # [enter, snapshot taken, bitvector launched, all launched, seen, done]
+        hs = [(x[1] - x[0]) / 1e3 for x in h]
+        hb = [(x[2] - x[1]) / 1e3 for x in h]
+        hl = [(x[3] - x[2]) / 1e3 for x in h]
+        hw = [(x[4] - x[3]) / 1e3 for x in h]
+        hd = [(x[5] - x[4]) / 1e3 for x in h]
         print(f"  bitvector kernel us: populate p50 {pct(kpop,.5):.2f}  AND p50 {pct(kand,.5):.2f}  "
               f"release+handoff p50 {pct(krel,.5):.2f}")
-        print(f"  host us: pre-launch p50 {pct(hl,.5):.2f}  wait-for-handoff p50 {pct(hw,.5):.2f}  "
-              f"post (data launch) p50 {pct(hd,.5):.2f}")
+        print(f"  host us p50: entry+snapshot {pct(hs,.5):.2f}  bitvector launch {pct(hb,.5):.2f}  "
+              f"data launch {pct(hl,.5):.2f}  wait-for-handoff {pct(hw,.5):.2f}  decode {pct(hd,.5):.2f}")
         for r in recs:
             raw = r["items"]
             if not raw:
