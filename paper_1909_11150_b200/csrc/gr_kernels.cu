@@ -592,14 +592,19 @@ __device__ __forceinline__ float grad_load1(const char *g, int64_t idx, bool f16
 // NEXT-2 epilogue (LARS needs ||g||^2 per tensor, dynamic loss scaling needs a non-finite
 // flag): accumulate the squares of the values as stored in the gradient
 // tensor and note any Inf/NaN. Per thread in registers; one warp reduction + atomic per piece.
-// Per lane the squares are summed in fp32 over one piece (a tensor's overlap with one warp
-// sub-item of the N=1 kernel: at most 8 vectors of 8 per lane at the default 2048-element
-// sub-item; with one staged sub-tile of the xfer kernel: at most 3), all terms non-negative,
-// so the partial's relative error stays below (7 + 8) * 2^-24 ~ 9e-7 (typically ~1e-7); the
-// warp's partials are then added in fp64 and accumulated per tensor in fp64 (R19).
-// One fp32 register instead of an fp64 pair helps the HBM-bound N=1 kernel keep its occupancy.
-struct GradStat {
-    float ss = 0.f;
+// Every 8-element buffer vector's squares are summed in fp32 (the same 8 elements on every rank
+// and path: vectors are 8-aligned in the fusion buffer). ACC = float (N=1 kernel): the vector
+// sums of one piece (a tensor's overlap with one warp sub-item: at most 8 per lane at the
+// default 2048-element sub-item) are added in fp32 too, all terms non-negative, relative error
+// below (7 + 8) * 2^-24 ~ 9e-7; one fp32 register instead of an fp64 pair keeps the HBM-bound
+// kernel at its occupancy, and with one rank there is no replica to agree with. ACC = double
+// (xfer kernel, N > 1): vector sums go straight into fp64, so ranks whose sub-tiles cut the
+// chunk differently (reduce-scatter owner vs all-gather) agree up to the fp64 summation order
+// (~1e-15 relative). The warp's partials are added in fp64 and accumulated per tensor in fp64
+// (R19).
+template <typename ACC>
+struct GradStatT {
+    ACC ss = 0;
     unsigned nf = 0;
     __device__ __forceinline__ void add8(const float (&x)[8], bool f16) {
         float s = 0.f;
@@ -609,11 +614,12 @@ struct GradStat {
             s = fmaf(v, v, s);
             nf |= !isfinite(v);
         }
-        ss += s;
+        ss += (ACC)s;
     }
     __device__ __forceinline__ void add1(float x, bool f16) {
         const float v = f16 ? __half2float(__float2half_rn(x)) : x;
-        ss = fmaf(v, v, ss);
+        if constexpr (sizeof(ACC) == 4) ss = fmaf(v, v, ss);
+        else ss += (ACC)(v * v);
         nf |= !isfinite(v);
     }
     // warp-collective: every lane of the warp must call it
@@ -626,10 +632,12 @@ struct GradStat {
             if (v != 0.0) atomicAdd(sumsq + tensor, v);
             if (anynf) atomicOr(nonfinite, 1);
         }
-        ss = 0.f;
+        ss = 0;
         nf = 0;
     }
 };
+using GradStat = GradStatT<float>;    // local_kernel (N = 1)
+using GradStatX = GradStatT<double>;  // xfer_kernel (N > 1)
 
 __device__ __forceinline__ void grad_store1(char *g, int64_t idx, bool f16, float x) {
     if (f16) *reinterpret_cast<__half *>(g + idx * 2) = __float2half_rn(x);
@@ -863,7 +871,7 @@ __device__ __forceinline__ void xf_consume(const DataParams &p, const XfMeta &m,
         // peer slot) every whole vector of an aligned gradient — the same split as the RS path
         // (body = n rounded down to 16 B), so statistics group elements identically on all ranks
         const int64_t nvec = (KIND == K_AG) ? (pc.galigned ? (pc.n >> 3) : 0) : (pc.body >> 3);
-        GradStat st;
+        GradStatX st;
         for (int64_t v = ct; v < nvec; v += XF_CONS) {
             const int64_t e = 8 * v, bi = pc.lo + e, ti = pc.toff + e;
             const int64_t so = (bi - sb) * B::ES;  // byte offset inside a peer slot
@@ -963,7 +971,7 @@ __device__ __forceinline__ void xf_nvls_reduce(const DataParams &p, const XfMeta
         const int64_t esz = pc.f16 ? 2 : 4;
         const bool galigned = ((reinterpret_cast<uintptr_t>(pc.g) + pc.toff * esz) & 15) == 0;
         const int64_t nv = (pc.n + 7) >> 3;  // buffer vectors (the last may cover padding)
-        GradStat st;
+        GradStatX st;
         constexpr int U = 4;                 // switch reductions in flight per thread
         for (int64_t v0 = ct; v0 < nv; v0 += (int64_t)XF_CONS * U) {
             float x[U][8];
