@@ -175,6 +175,36 @@ def run_reference(args):
     print(json.dumps(out), flush=True)
 
 
+def nvlink_read(index: int):
+    try:
+        sys.path.insert(0, os.path.join(ROOT, "tools"))
+        import nvlink_counters
+        return nvlink_counters.read(index)
+    except Exception as e:  # noqa: BLE001 — the counters are evidence, not the measurement
+        return {"error": repr(e)}
+
+
+def nvlink_summary(a, b, steps: int, S: int, N: int, dev):
+    """Per-GPU NVLink bytes per step from NVML's cumulative counters, gathered from every rank,
+    set against the algorithmic 2(N-1)/N*S per direction (two-shot / one-shot at N=2)."""
+    import torch
+    import torch.distributed as dist
+    keys = ("data_tx", "data_rx", "link_tx", "link_rx")
+    row = []
+    for k in keys:
+        ok = isinstance(a, dict) and isinstance(b, dict) and a.get(k) is not None and b.get(k) is not None
+        row.append(float(b[k] - a[k]) / steps if ok else -1.0)
+    t = torch.tensor(row, dtype=torch.float64, device=dev)
+    allr = [torch.empty_like(t) for _ in range(N)]
+    dist.all_gather(allr, t)
+    per_rank = [[None if x < 0 else x for x in r.tolist()] for r in allr]
+    alg = 2 * (N - 1) / N * S
+    return {"per_rank_per_step": [dict(zip(keys, r)) for r in per_rank],
+            "units": "data_*: NVML THROUGHPUT_DATA (KiB per NVML); link_*: sum of per-link COUNT_*_BYTES",
+            "algorithmic_bytes_per_direction_per_step": alg, "steps": steps,
+            "note": "ratio counted/algorithmic needs the unit scale measured by tools/nvlink_counters.py"}
+
+
 def _max_over(x: float, dev) -> float:
     import torch
     import torch.distributed as dist
@@ -282,9 +312,11 @@ def main():
         # step count comes from the max-over-ranks time, so every rank runs the same number of
         # collective steps.
         n_soak = int(min(20000, max(1, 1000.0 / max(1e-3, max_over_ranks(ms_local)))))
+        nvl0 = nvlink_read(local) if N > 1 else None
         for _ in range(n_soak):
             one_step()
         torch.cuda.synchronize()
+        nvl1 = nvlink_read(local) if N > 1 else None
     barrier()
     st = st_timed  # counters of exactly the K timed steps (the clock soak follows)
     ctx_nvls = "%s (%s)" % ctx.nvls() if N > 1 else None
@@ -438,6 +470,9 @@ def main():
         cpu = cpu_oracle_leg(N, args.cpu_seconds, buf16)
         cpu.pop("seconds_per_step_sample", None)
 
+    nvlink = None
+    if N > 1:  # NVLink payload counters over the soak's identical steps, per step, vs 2(N-1)/N*S
+        nvlink = nvlink_summary(nvl0, nvl1, n_soak, S, N, dev)
     if rank == 0:
         out = {"metric": METRIC, "value": round(value, 3), "unit": "GB/s", "n_gpus": N, "steps": args.steps,
                "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "weak",
@@ -457,6 +492,8 @@ def main():
                "gpu_launches": launches, "launches_per_step": launches / args.steps,
                "bitvector_kernel_us": round(bv_ms * 1e3, 2),
                "roofline": roof, "clocks": clk.summary(), "e2e": e2e, "cpu_baseline": cpu}
+        if nvlink is not None:
+            out["nvlink_counters"] = nvlink
         out.update(extras)
         print(json.dumps(out), flush=True)
     ctx.gr_finalize()
@@ -572,6 +609,47 @@ def run_extras(args, ctx, grads, ptrs, tensor_order, f, N, rank, local, dev, com
     torch.cuda.synchronize()
     out["ms_per_step_with_grad_stats"] = round(max_over_ranks(a0.elapsed_time(a1) / 10), 4)
     ctx.gr_enable_grad_stats(False)
+
+    # ---- cfg3 per-group end-to-end bus bandwidth: one group released per cycle, group by group
+    # (mark its tensors -> gr_step releases it -> its fused pack/reduce/unpack), timed with events
+    # on the compute stream from before the marks to after gr_released_wait_async ----
+    if N > 1:
+        members = {}
+        for t in tensor_order:
+            members.setdefault(int(f.group_of[t]), []).append(t)
+        gorder = list(dict.fromkeys(int(f.group_of[t]) for t in tensor_order))  # reverse-layer release
+        per = {g: [] for g in gorder}
+        pb_ = 2 if args.buffer == "f16" else 4
+        for rep in range(6):
+            evs = []
+            barrier()
+            torch.cuda.synchronize()
+            for g in gorder:
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(compute)
+                ids = members[g]
+                ctx.gr_mark_ready_batch(ids, [ptrs[t] for t in ids])
+                rel, _complete, _A, _ = ctx.gr_step(bits=False)
+                assert rel == [g], (rel, g)
+                ctx.gr_released_wait_async(compute.cuda_stream)
+                e1.record(compute)
+                evs.append((g, e0, e1))
+            ctx.gr_wait()
+            torch.cuda.synchronize()
+            if rep >= 1:
+                for g, e0, e1 in evs:
+                    per[g].append(e0.elapsed_time(e1))
+        rows = []
+        for g in sorted(per):
+            ms_g = max_over_ranks(statistics.median(per[g]))
+            Sg = int(sum(int(f.numel[t]) for t in members[g])) * pb_
+            rows.append({"group": g, "bytes": Sg, "ms": round(ms_g, 4),
+                         "busbw_GBps": round(Sg * 2 * (N - 1) / N / (ms_g * 1e-3) / 1e9, 1)})
+        out["per_group_e2e"] = {"groups": rows,
+                                "what": "one group per cycle in reverse-layer order: mark its tensors -> gr_step -> "
+                                        "fused pack/reduce/unpack; events on the compute stream around marks..."
+                                        "gr_released_wait_async; median of 5 steps, max over ranks; busbw = "
+                                        "S_g*2(N-1)/N/t (SURVEY.md §8(d) cfg3: >=720 GB/s target for g4/g5/g6)"}
 
     # ---- bitvector-only cycle latency (no tensor ready: pure coordination round) ----
     lat = []

@@ -114,10 +114,13 @@ struct DataParams {
     const int32_t *group_spc;          // [G]: local-kernel sub-items per full chunk of the group
     const uint64_t *dev_ptr;           // [T]
     char *buf[GR_MAX_RANKS];           // every rank's fusion buffer for this step parity
-    char *rsb[GR_MAX_RANKS];           // push two-shot: every rank's reduce-scatter receive slots
-                                       // [N-1][buffer] (source s lands in slot s<owner ? s : s-1)
-    int32_t push;                      // two-shot by remote stores (1) or remote loads (0)
+    char *rsb[GR_MAX_RANKS];           // push: every rank's receive slots [N-1][buffer] for packed
+                                       // chunks (source s lands in slot s<receiver ? s : s-1)
+    int32_t push;                      // one-/two-shot by TMA bulk stores into peers (1) or by TMA
+                                       // bulk loads from peers (0)
     int64_t rsb_stride;                // bytes between receive slots (one fusion buffer)
+    int64_t out_bytes;                 // push: bytes of one shared-memory output tile
+    int32_t nout;                      // push: output tiles (2..4) after the stage ring
     char *nvls_uc;                     // NVLS: this rank's copy of the multicast buffer (parity), or null
     char *nvls_mc;                     // NVLS: the multicast view of it (multimem.*), or null
     uint32_t *pack_flag[GR_MAX_RANKS]; // every rank's pack flags [C][N] for this parity

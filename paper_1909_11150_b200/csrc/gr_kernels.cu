@@ -754,6 +754,8 @@ __global__ void __launch_bounds__(LC_THREADS, GR_LC_MINB) local_kernel(const __g
 constexpr int XF_THREADS = 512;
 constexpr int XF_CONS = XF_THREADS - 64;  // warp 0 producer, warp 1 publisher, warps 2.. consumers
 constexpr int XF_PUB = 8;                   // publication ring (chunk flags waiting for the fence)
+constexpr int XF_OUT = 4;                   // push: max output tiles (runtime count: p.nout)
+constexpr int XF_PF = 8;                    // push: chunk flags deferred until their bulk stores complete
 constexpr int XF_STAGES = 8;  // max ring depth (runtime depth: p.nstages)
 enum { K_PACK = 0, K_RED = 1, K_RS = 2, K_AG = 3, K_NRS = 5, K_STOP = 4 };
 
@@ -778,6 +780,37 @@ __device__ __forceinline__ void mbar_wait(uint64_t *b, uint32_t parity) {
 __device__ __forceinline__ void bulk_g2s(void *dst_smem, const void *src, uint32_t bytes, uint64_t *bar) {
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
                  ::"r"(smem_u32(dst_smem)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+
+// push path: shared-memory output tile -> (peer) global memory, tracked in bulk groups of the
+// issuing thread (the publisher lane)
+__device__ __forceinline__ void bulk_s2g(void *dst, const void *src_smem, uint32_t bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
+                 ::"l"(dst), "r"(smem_u32(src_smem)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+// at most K of this thread's bulk groups still reading shared memory (K: immediate)
+__device__ __forceinline__ void bulk_wait_read(int k) {
+    switch (k) {
+        case 0: asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); break;
+        case 1: asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); break;
+        case 2: asm volatile("cp.async.bulk.wait_group.read 2;" ::: "memory"); break;
+        default: asm volatile("cp.async.bulk.wait_group.read 3;" ::: "memory"); break;
+    }
+}
+// at most K of this thread's bulk groups not yet complete (their writes performed)
+__device__ __forceinline__ void bulk_wait(int k) {
+    switch (k) {
+        case 0: asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); break;
+        case 1: asm volatile("cp.async.bulk.wait_group 1;" ::: "memory"); break;
+        default: asm volatile("cp.async.bulk.wait_group 2;" ::: "memory"); break;
+    }
+}
+__device__ __forceinline__ bool mbar_test(uint64_t *b, uint32_t parity) {
+    uint32_t done;
+    asm volatile("{ .reg .pred p; mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                 : "=r"(done) : "r"(smem_u32(b)), "r"(parity) : "memory");
+    return done != 0;
 }
 
 // thread 0 of the producer: wait until *flag == epoch (or abort / timeout); false = abort
@@ -876,7 +909,7 @@ __device__ __forceinline__ void xf_consume(const DataParams &p, const XfMeta &m,
             const int64_t e = 8 * v, bi = pc.lo + e, ti = pc.toff + e;
             const int64_t so = (bi - sb) * B::ES;  // byte offset inside a peer slot
             float acc[8];
-            if constexpr (KIND == K_PACK) {  // own_buf: this rank's buffer, or (push) the owner's slot
+            if constexpr (KIND == K_PACK) {  // own_buf: this rank's buffer, or (push) the output tile
                 lds_grad8(gs + e * esz, pc.f16, acc);
                 B::store(own_buf, bi, B::from_f32(acc));
                 continue;
@@ -901,15 +934,9 @@ __device__ __forceinline__ void xf_consume(const DataParams &p, const XfMeta &m,
 #pragma unroll
                 for (int i = 0; i < 8; ++i) acc[i] = acc[i] * p.inv_n;
                 typename B::Raw out = B::from_f32(acc);
-                if constexpr (KIND == K_RS) {
-                    if (p.push) {  // push the reduced chunk into every peer's buffer
-#pragma unroll
-                        for (int q = 0; q < GR_MAX_RANKS; ++q)
-                            if (q < p.N && q != p.rank) B::store(p.buf[q], bi, out);
-                    } else {
-                        B::store(own_buf, bi, out);
-                    }
-                }
+                // own_buf: this rank's fusion buffer (peers pull the reduced chunk), or (push) the
+                // shared-memory output tile the publisher bulk-stores into every peer's buffer
+                if constexpr (KIND == K_RS) B::store(own_buf, bi, out);
             }
             grad_store(pc.g, ti, pc.f16, acc);
             if (STATS) st.add8(acc, pc.f16);
@@ -935,14 +962,7 @@ __device__ __forceinline__ void xf_consume(const DataParams &p, const XfMeta &m,
                     a = (r == 0) ? x : a + x;
                 }
                 y = B::round1(a * p.inv_n);
-                if constexpr (KIND == K_RS) {
-                    if (p.push) {
-                        for (int q = 0; q < p.N; ++q)
-                            if (q != p.rank) B::store1(p.buf[q], bi, y);
-                    } else {
-                        B::store1(own_buf, bi, y);
-                    }
-                }
+                if constexpr (KIND == K_RS) B::store1(own_buf, bi, y);
             }
             grad_store1(pc.g, ti, pc.f16, y);
             if (STATS) st.add1(y, pc.f16);
@@ -1018,6 +1038,9 @@ __device__ __forceinline__ void xfer_body(const DataParams &p, const int cta, co
     __shared__ __align__(8) uint64_t full[XF_STAGES], empty[XF_STAGES];
     __shared__ __align__(8) uint64_t pub_full[XF_PUB], pub_empty[XF_PUB];
     __shared__ int pub_kind[XF_PUB], pub_chunk[XF_PUB];
+    __shared__ __align__(8) uint64_t out_full[XF_OUT], out_empty[XF_OUT];
+    __shared__ int out_kind[XF_OUT], out_chunk[XF_OUT], out_last[XF_OUT], out_nb[XF_OUT];
+    __shared__ int64_t out_sb[XF_OUT];
     __shared__ XfMeta meta[XF_STAGES];
     __shared__ int s_cum[XF_RCACHE], s_cb[XF_RCACHE];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -1031,6 +1054,10 @@ __device__ __forceinline__ void xfer_body(const DataParams &p, const int cta, co
         for (int s = 0; s < XF_PUB; ++s) {
             mbar_init(&pub_full[s], XF_CONS / 32);
             mbar_init(&pub_empty[s], 1);
+        }
+        for (int s = 0; s < XF_OUT; ++s) {
+            mbar_init(&out_full[s], XF_CONS / 32);
+            mbar_init(&out_empty[s], 1);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -1058,6 +1085,10 @@ __device__ __forceinline__ void xfer_body(const DataParams &p, const int cta, co
         return s_cb[lo] + (i - s_cum[lo]);
     };
     const int lag1 = p.lag1, lag2 = (ALGO == ALGO_ONESHOT) ? p.lag1 : p.lag2;
+    // push (one-/two-shot): packed and reduced sub-tiles leave through shared-memory output tiles
+    // that the publisher bulk-stores into the peers (NVLS keeps its multicast path)
+    const bool pushed = p.push && ALGO != ALGO_NVLS;
+    char *const out_base = xsm + (size_t)nst * stage_bytes;
     const int nk = total > 0 ? total + lag2 : 0;  // queue triples
     if (warp == 0) {
         // ---------------- producer warp: lane 0 owns the queue, barriers and flag waits;
@@ -1070,7 +1101,6 @@ __device__ __forceinline__ void xfer_body(const DataParams &p, const int cta, co
         const long long prof_t0 = clock64();
         // stream chunk c as sub-tiles of `sub` elements. src: 0 none (PACK), 1 every peer
         // (RED/RS), 2 the owner (AG); grads: stage own gradient pieces (PACK/RED/RS)
-        const bool pushed = p.push && ALGO == ALGO_TWOSHOT;
         auto produce = [&](int kind, int item, int c, int64_t sub, int src, int owner, bool grads) {
             const Chunk ch = p.chunks[c];
             const int nseg = ch.seg_end - ch.seg_begin;
@@ -1231,7 +1261,74 @@ __device__ __forceinline__ void xfer_body(const DataParams &p, const int cta, co
         // the consumers' stores are release-ordered before their arrive), makes them visible at
         // system scope (fence.sc.sys waits for the stores) and pushes the chunk flags to the
         // peers — the fence latency never stalls the consumer pipeline.
-        if (lane == 0) {
+        if (lane == 0 && pushed) {
+            // push: issue each finished output tile as TMA bulk stores into the peers (one bulk
+            // group per tile), recycle a tile once its stores have read it, and publish a
+            // chunk's flag only after the stores of its last tile have COMPLETED (deferred: the
+            // flag waits for completion two tiles later, or at once when no tile is ready).
+            int j = 0, issued = 0;
+            uint32_t ph = 0;
+            int pf_kind[XF_PF], pf_chunk[XF_PF], pf_group[XF_PF];
+            int pf_n = 0;
+            const int keep = p.nout - 1;  // groups allowed to still read shared memory
+            auto flags = [&](int upto) {  // publish the deferred flags of groups <= upto
+                asm volatile("fence.proxy.async.global;" ::: "memory");
+                fence_sys();
+                int k = 0;
+                for (int i = 0; i < pf_n; ++i) {
+                    if (pf_group[i] > upto) { pf_kind[k] = pf_kind[i]; pf_chunk[k] = pf_chunk[i]; pf_group[k] = pf_group[i]; ++k; continue; }
+                    const int c = pf_chunk[i];
+                    if (pf_kind[i] == K_RS) {
+                        for (int q = 0; q < p.N; ++q)
+                            if (q != p.rank) st_relaxed_sys32(p.rs_flag[q] + c, p.epoch);
+                    } else if (ALGO == ALGO_TWOSHOT) {
+                        st_relaxed_sys32(p.pack_flag[c % p.N] + (size_t)c * p.N + p.rank, p.epoch);
+                    } else {  // one-shot: every receiver, and this rank (its RED(c) overwrites g after PACK(c) read it)
+                        for (int q = 0; q < p.N; ++q) st_relaxed_sys32(p.pack_flag[q] + (size_t)c * p.N + p.rank, p.epoch);
+                    }
+                }
+                pf_n = k;
+            };
+            for (;;) {
+                if (!mbar_test(&out_full[j], ph)) {
+                    if (pf_n) { bulk_wait(0); flags(issued); }  // idle: nothing may wait on a deferred flag
+                    mbar_wait(&out_full[j], ph);
+                }
+                const int kind = out_kind[j];
+                if (kind == K_STOP) break;
+                const int c = out_chunk[j];
+                const int64_t sb = out_sb[j];
+                const uint32_t nb = (uint32_t)out_nb[j];
+                const char *tile = out_base + (size_t)j * p.out_bytes;
+                if (kind == K_PACK && ALGO == ALGO_TWOSHOT) {  // into the owner's receive slot
+                    const int o = c % p.N;
+                    bulk_s2g(p.rsb[o] + (size_t)(p.rank < o ? p.rank : p.rank - 1) * p.rsb_stride + sb * B::ES, tile, nb);
+                } else {
+                    for (int q = 0; q < p.N; ++q) {
+                        if (q == p.rank) continue;
+                        char *dst = kind == K_PACK ? p.rsb[q] + (size_t)(p.rank < q ? p.rank : p.rank - 1) * p.rsb_stride
+                                                   : p.buf[q];  // RS: the reduced chunk into every peer's buffer
+                        bulk_s2g(dst + sb * B::ES, tile, nb);
+                    }
+                }
+                bulk_commit();
+                ++issued;
+                if (out_last[j]) {
+                    if (pf_n == XF_PF) { bulk_wait(0); flags(issued - 1); }
+                    pf_kind[pf_n] = kind;
+                    pf_chunk[pf_n] = c;
+                    pf_group[pf_n] = issued;
+                    ++pf_n;
+                }
+                // the tile of group issued-keep has been read: hand it back to the consumers
+                bulk_wait_read(keep);
+                if (issued - keep >= 1) mbar_arrive(&out_empty[(issued - keep - 1) % p.nout]);
+                if (pf_n && pf_group[0] <= issued - 2) { bulk_wait(2); flags(issued - 2); }
+                if (++j == p.nout) { j = 0; ph ^= 1; }
+            }
+            bulk_wait(0);
+            if (pf_n) flags(issued);
+        } else if (lane == 0) {
             for (int ps = 0, ph = 0;; ) {
                 mbar_wait(&pub_full[ps], ph);
                 const int kind = pub_kind[ps], c = pub_chunk[ps];
@@ -1255,6 +1352,8 @@ __device__ __forceinline__ void xfer_body(const DataParams &p, const int cta, co
         uint32_t ph = 0;
         int ps = 0;
         uint32_t pph = 1;  // publication slots start free
+        int ot = 0;
+        uint32_t oph = 1;  // output tiles start free
         long long prof_full = 0, prof_flag = 0;
         const long long prof_t0 = clock64();
         // hand a finished chunk (or the stop message) to the publisher
@@ -1281,24 +1380,39 @@ __device__ __forceinline__ void xfer_body(const DataParams &p, const int cta, co
             const int kind = m.kind;
             if (kind == K_STOP) break;
             const int item = m.item, c = m.chunk, last = m.last;
+            const int64_t msb = m.sb, mse = m.se;
             const char *st = xsm + (size_t)stage * stage_bytes;
             char *own = ALGO == ALGO_NVLS ? p.nvls_uc : p.buf[p.rank];  // this rank's fusion buffer
-            if (kind == K_PACK) {
-                char *dst = own;  // push two-shot: straight into the owner's receive slot (NVLink)
-                if (ALGO == ALGO_TWOSHOT && p.push) {
-                    const int o = c % p.N;
-                    dst = p.rsb[o] + (size_t)(p.rank < o ? p.rank : p.rank - 1) * p.rsb_stride;
-                }
-                xf_consume<BT, K_PACK, STATS>(p, m, st, 0, st, ct, dst);
+            // push: PACK / RS results go to an output tile (indexed like the buffer, from msb)
+            const bool tile = pushed && (kind == K_PACK || kind == K_RS);
+            if (tile) {
+                if (lane == 0) mbar_wait(&out_empty[ot], oph);
+                __syncwarp();
+                own = out_base + (size_t)ot * p.out_bytes - msb * B::ES;
             }
+            if (kind == K_PACK) xf_consume<BT, K_PACK, STATS>(p, m, st, 0, st, ct, own);
             else if (kind == K_RED) xf_consume<BT, K_RED, STATS>(p, m, st, p.slot_bytes_red, st + gslot_off, ct, own);
             else if (kind == K_RS) xf_consume<BT, K_RS, STATS>(p, m, st, p.slot_bytes_red, st + gslot_off, ct, own);
             else if (kind == K_NRS) xf_nvls_reduce<BT, STATS>(p, m, ct);
             else xf_consume<BT, K_AG, STATS>(p, m, st, 0, st, ct, own);
+            // generic-proxy tile writes -> visible to the bulk store (async proxy) the publisher issues
+            if (tile) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             // the stage is free once every consumer warp has read it
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[stage]);
-            if (last && (kind == K_PACK || kind == K_RS || kind == K_NRS)) publish(kind, c);
+            if (tile) {
+                if (ct == 0) {
+                    out_kind[ot] = kind;
+                    out_chunk[ot] = c;
+                    out_last[ot] = last;
+                    out_sb[ot] = msb;
+                    out_nb[ot] = (int)(((mse - msb) * B::ES + 15) & ~(int64_t)15);
+                }
+                if (lane == 0) mbar_arrive(&out_full[ot]);  // release: this warp's tile writes, ct 0's meta
+                if (++ot == p.nout) { ot = 0; oph ^= 1; }
+            } else if (last && (kind == K_PACK || kind == K_RS || kind == K_NRS)) {
+                publish(kind, c);
+            }
             if (p.trace && last && ct == 0) {
                 uint32_t smid;
                 asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
@@ -1307,7 +1421,14 @@ __device__ __forceinline__ void xfer_body(const DataParams &p, const int cta, co
             }
             if (++stage == nst) { stage = 0; ph ^= 1; }
         }
-        publish(K_STOP, 0);
+        if (pushed) {  // stop message through the output ring (the publisher loops on it)
+            if (lane == 0) mbar_wait(&out_empty[ot], oph);
+            __syncwarp();
+            if (ct == 0) out_kind[ot] = K_STOP;
+            if (lane == 0) mbar_arrive(&out_full[ot]);
+        } else {
+            publish(K_STOP, 0);
+        }
         if (p.trace && ct == 0) {
             uint64_t *pr = p.trace + (size_t)3 * p.trace_items + (size_t)cta * 8;
             pr[3] = (uint64_t)(clock64() - prof_t0);
@@ -1351,11 +1472,16 @@ static void xfer_attrs() {
     }
 }
 
+// dynamic shared memory of the xfer kernel: the stage ring, then (push) the output tiles
+static size_t xfer_smem(const DataParams &p) {
+    return (size_t)p.nstages * p.stage_bytes + (p.push ? (size_t)p.nout * p.out_bytes : 0);
+}
+
 template <typename BT, bool STATS>
 static int launch_data_t(const DataParams &p, int local, int ctas, cudaStream_t s) {
     xfer_attrs<BT, STATS>();
     if (local) local_kernel<BT, STATS><<<ctas, LC_THREADS, 0, s>>>(p);
-    else xfer_kernel<BT, STATS><<<ctas, XF_THREADS, (size_t)p.nstages * p.stage_bytes, s>>>(p);
+    else xfer_kernel<BT, STATS><<<ctas, XF_THREADS, xfer_smem(p), s>>>(p);
     return (int)cudaGetLastError();
 }
 
@@ -1370,7 +1496,7 @@ static int launch_data_v_t(const DataParamsV &pv, cudaStream_t s) {
     xfer_attrs<BT, STATS>();
     int r0 = 0;  // the stage ring is the same on every rank: take a present rank's
     while (r0 < pv.N - 1 && ((pv.absent >> r0) & 1u)) ++r0;
-    xfer_kernel_v<BT, STATS><<<pv.N * pv.per, XF_THREADS, (size_t)pv.r[r0].nstages * pv.r[r0].stage_bytes, s>>>(pv);
+    xfer_kernel_v<BT, STATS><<<pv.N * pv.per, XF_THREADS, xfer_smem(pv.r[r0]), s>>>(pv);
     return (int)cudaGetLastError();
 }
 

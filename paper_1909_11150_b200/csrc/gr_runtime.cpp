@@ -160,6 +160,7 @@ struct gr_ctx {
     int data_ctas_full[4] = {0, 0, 0, 0};  // every SM (drain cycles)
     int lag1 = 0, lag2 = 0;  // GR_LAG1 / GR_LAG2 overrides (tuning)
     int nstages = 4, stage_kb = 48;  // GR_STAGES / GR_STAGE_KB overrides (tuning)
+    int nout = 2, out_kb = 24;       // push: output tiles (GR_OUT_TILES / GR_OUT_KB overrides)
     int64_t lc_sub = 2048;           // local kernel sub-item (GR_LC_SUB, tuning; measured best)
     std::vector<void *> async_streams;  // distinct streams of this step's gr_mark_ready_async calls
 
@@ -534,9 +535,18 @@ int setup_local(gr_ctx *c) {
         q == cudaDriverEntryPointSuccess)
         c->write_value32 = (PFN_writeValue32)fn;
 
+    // 208 KB of dynamic shared memory per CTA: the stage ring, and with push the output tiles
+    // (default 4 x 40 KB stages + 2 x 24 KB tiles)
+    if (c->push) {
+        c->stage_kb = 40;
+        if (const char *no = getenv("GR_OUT_TILES")) c->nout = std::max(2, std::min(4, atoi(no)));
+        if (const char *ok = getenv("GR_OUT_KB")) c->out_kb = std::max(4, atoi(ok) / 4 * 4);
+        if (c->nout * c->out_kb > 104) c->out_kb = 104 / c->nout / 4 * 4;
+    }
     if (const char *ns = getenv("GR_STAGES")) c->nstages = std::max(2, std::min(8, atoi(ns)));
     if (const char *sk = getenv("GR_STAGE_KB")) c->stage_kb = std::max(8, atoi(sk));
-    if (c->nstages * c->stage_kb > 208) c->stage_kb = 208 / c->nstages / 16 * 16;
+    const int budget = 208 - (c->push ? c->nout * c->out_kb : 0);
+    if (c->nstages * c->stage_kb > budget) c->stage_kb = budget / c->nstages / 16 * 16;
     if (const char *tp = getenv("GR_TRACE")) {
         if (*tp) {
             c->trace_path = std::string(tp) + ".rank" + std::to_string(c->rank) + ".jsonl";
@@ -1210,7 +1220,11 @@ static int step_impl(gr_ctx *c, int32_t *released, gr_cycle_info *info, uint32_t
         sr = std::max<int64_t>(256, std::min<int64_t>(sr, cmax));
         d.sub_red = sr;
         d.slot_bytes_red = sr * es;
-        d.sub_pack = std::max<int64_t>(256, std::min<int64_t>(stage / 4 / 256 * 256, cmax));
+        int64_t spk = stage / 4 / 256 * 256;  // fp32 gradients staged
+        if (c->push) spk = std::min<int64_t>(spk, (int64_t)c->out_kb * 1024 / es / 256 * 256);  // one output tile
+        d.sub_pack = std::max<int64_t>(256, std::min<int64_t>(spk, cmax));
+        d.out_bytes = (int64_t)c->out_kb * 1024;
+        d.nout = c->nout;
         d.sub_ag = std::max<int64_t>(256, std::min<int64_t>(stage / es / 256 * 256, cmax));
         d.one_shot_max_bytes = c->one_shot_max_bytes;
         d.push = c->push ? 1 : 0;

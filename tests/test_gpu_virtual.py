@@ -167,6 +167,78 @@ def test_virtual_many_steps_same_contexts(gpu, n):
             c.gr_finalize()
 
 
+# ------------------------------------------------------------------ push data path (GR_PUSH=1)
+
+@pytest.fixture
+def push_mode(monkeypatch):
+    """Contexts created inside the test use the push data path: packed sub-tiles and reduced
+    chunks leave each rank through shared-memory output tiles that TMA bulk-stores into the
+    peers' receive slots / fusion buffers."""
+    monkeypatch.setenv("GR_PUSH", "1")
+    yield
+
+
+@pytest.mark.parametrize("n", NS)
+def test_virtual_push_edge_both_algorithms(gpu, n, push_mode):
+    """Push path, one-shot and two-shot forced: ragged sizes, tensors spanning many chunks and
+    sub-tiles (the output-tile ring wraps many times), fp16 gradients, both buffer precisions,
+    integer payloads — bit-exact against oracle.emulate, replicas identical."""
+    from paper_1909_11150_b200 import GR_ALGO_ONESHOT, GR_ALGO_TWOSHOT
+    from tests.parity_lib import run_virtual_case
+    for seed in range(2):
+        rng = np.random.default_rng(100 + seed)
+        T = int(rng.integers(1, 24))
+        G = int(rng.integers(1, T + 1))
+        numel = rng.integers(1, 200000, size=T).astype(np.int64)
+        numel[rng.integers(0, T)] = int(rng.integers(1, 9))
+        case = Case(n, numel, random_partition(T, G, rng), random_mark_schedule(n, T, seed, 3), seed)
+        gf = (rng.random(T) < 0.3).tolist()
+        for buf16 in (True, False):
+            chunk = int(rng.choice([1024, 4096, 32768]))
+            out = run_virtual_case(case, seed, gpu, buf16, grad_f16=gf, chunk_elems=chunk,
+                                   one_shot_max_bytes=TWO_SHOT)
+            assert _algos(out) == {GR_ALGO_TWOSHOT}
+            out = run_virtual_case(case, seed, gpu, buf16, grad_f16=gf, chunk_elems=chunk,
+                                   one_shot_max_bytes=ONE_SHOT)
+            assert _algos(out) == {GR_ALGO_ONESHOT}
+        run_virtual_case(case, seed, gpu, True, kind="int", one_shot_max_bytes=TWO_SHOT)
+    for seed in range(4):  # configs[0]'s shape
+        run_virtual_case(cfg1_case(seed, N=n), seed, gpu, seed % 2 == 0, timeout_ms=20000)
+
+
+@pytest.mark.parametrize("n", [2, 4])
+def test_virtual_push_numeric_edges_stats_steps(gpu, n, push_mode):
+    """Push path: numeric edge cases (R8 range, subnormals, specials, cancellation) and the
+    NEXT-2 statistics for both algorithms, five steps on the same contexts (receive slots and
+    flags double-buffered by step parity), the fcn220m set at full size two-shot."""
+    from paper_1909_11150_b200 import GR_F16, virtual_world
+    from tests.parity_lib import run_case_on_rank, run_ranks, run_virtual_case
+    rng = np.random.default_rng(150 + n)
+    T = 7
+    numel = rng.integers(1, 120000, size=T).astype(np.int64)
+    case = Case(n, numel, random_partition(T, 3, rng), random_mark_schedule(n, T, 150 + n, 2), 150 + n)
+    gf = [t % 3 == 0 for t in range(T)]
+    for buf16 in (True, False):
+        for osm in (TWO_SHOT, ONE_SHOT):
+            run_virtual_case(case, 150 + n, gpu, buf16, grad_f16=gf, kind="edge", one_shot_max_bytes=osm,
+                             chunk_elems=4096)
+            run_virtual_case(case, 150 + n, gpu, buf16, grad_f16=gf, stats=True, one_shot_max_bytes=osm)
+    base = cfg1_case(9, N=n)
+    ctxs = virtual_world(world_size=n, device=0, numel=base.numel, group_of=base.group_of, buffer_dtype=GR_F16,
+                         one_shot_max_bytes=TWO_SHOT, chunk_elems=256)
+    try:
+        for step in range(5):
+            c = Case(n, base.numel, base.group_of, random_mark_schedule(n, base.T, 300 + step, 3), 300 + step)
+            hs = run_ranks(n, lambda r: run_case_on_rank(ctxs[r], c, r, 300 + step, gpu, True)[1])
+            assert len(set(hs)) == 1
+    finally:
+        for cx in ctxs:
+            cx.gr_finalize()
+    f = fcn220m()
+    mark = reverse_layer_schedule(len(f.layers), n, f.release_order, layers_per_cycle=1, jitter_seed=n, max_shift=2)
+    run_virtual_case(Case(n, f.numel, f.group_of, mark, 60 + n), 60 + n, gpu, True, one_shot_max_bytes=TWO_SHOT)
+
+
 # ------------------------------------------------------------------ failure paths (§8(b) errors)
 
 def _tiny_world(n, **kw):

@@ -1,8 +1,8 @@
 """cfg4 (BASELINE.json configs[3]): bitvector-only cycle latency, T = 64 .. 65,536.
 
-  torchrun --nproc-per-node N tools/bench_cfg4.py [--cycles 2000] [--skew-us 0,10,100]
+  torchrun --nproc-per-node N tools/bench_cfg4.py [--cycles 10000] [--skew-us 0,10,100]
 
-T tensors of 8 elements, G = T/8 contiguous groups of 8; rank r marks in reverse order
+T = 2^6 .. 2^16 (11 points) tensors of 8 elements, G = T/8 contiguous groups of 8; rank r marks in reverse order
 rotated by r*T/N ("adversarial skew": a group completes only when the slowest rank's
 rotation reaches it), T/16 marks per cycle. The last rank is a straggler that enters
 gr_step delta us late every cycle. Reported per T: host latency of gr_step (p50/p99; for
@@ -29,7 +29,9 @@ def pct(xs, q):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--cycles", type=int, default=2000)
+    ap.add_argument("--cycles", type=int, default=10000)
+    ap.add_argument("--baseline-cycles", type=int, default=10000)
+    ap.add_argument("--tstep", type=int, default=2, help="T multiplier between points (2: all 11)")
     ap.add_argument("--skew-us", default="0,10,100")
     ap.add_argument("--tmax", type=int, default=65536)
     ap.add_argument("--tmin", type=int, default=64)
@@ -107,7 +109,7 @@ def main():
                 print(json.dumps(out), flush=True)
         ctx.gr_finalize()
         if a.no_baselines:
-            T *= 4
+            T *= a.tstep
             continue
         # baselines on the same box
         flags = torch.ones(T, dtype=torch.uint8, device=dev)
@@ -115,14 +117,15 @@ def main():
             dist.all_reduce(flags, op=dist.ReduceOp.MIN)
         torch.cuda.synchronize()
         nl = []
-        for _ in range(300):
+        nb = max(300, a.baseline_cycles)
+        for _ in range(nb):
             t0 = time.perf_counter()
             dist.all_reduce(flags, op=dist.ReduceOp.MIN)
             flags.cpu()  # the host needs the result, as gr_step's caller does
             nl.append((time.perf_counter() - t0) * 1e6)
         words = torch.ones((T + 2 + 31) // 32, dtype=torch.int32)
         gl = []
-        for i in range(300):
+        for i in range(nb):
             t0 = time.perf_counter()
             dist.all_reduce(words, op=dist.ReduceOp.BAND, group=gloo)
             gl.append((time.perf_counter() - t0) * 1e6)
@@ -131,7 +134,7 @@ def main():
         mw = MasterWorker(rank, N, case.group_of, pg=gloo)
         ml, mcyc = [], 0
         dist.barrier(group=gloo)
-        while mcyc < min(a.cycles, 600):
+        while mcyc < a.baseline_cycles:
             c = 0
             while True:
                 t0 = time.perf_counter()
@@ -141,15 +144,19 @@ def main():
                 mcyc += 1
                 if complete:
                     break
-        mw_p50 = torch.tensor([pct(ml, 0.5)], dtype=torch.float64)
-        dist.all_reduce(mw_p50, op=dist.ReduceOp.MAX, group=gloo)
+        mw_p = torch.tensor([pct(ml, 0.5), pct(ml, 0.99)], dtype=torch.float64)
+        dist.all_reduce(mw_p, op=dist.ReduceOp.MAX, group=gloo)
         if rank == 0:
             print(json.dumps({"T": T, "N": N, "baseline": True,
                               "nccl_min_u8_us_p50": round(pct(nl[50:], 0.5), 2),
+                              "nccl_min_u8_us_p99": round(pct(nl[50:], 0.99), 2),
                               "gloo_band_u32_us_p50": round(pct(gl[50:], 0.5), 2),
-                              "master_worker_us_p50": round(float(mw_p50), 2),
+                              "gloo_band_u32_us_p99": round(pct(gl[50:], 0.99), 2),
+                              "baseline_cycles": nb,
+                              "master_worker_us_p50": round(float(mw_p[0]), 2),
+                              "master_worker_us_p99": round(float(mw_p[1]), 2),
                               "master_worker_cycles": len(ml)}), flush=True)
-        T *= 4
+        T *= a.tstep
     dist.destroy_process_group()
 
 
