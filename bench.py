@@ -189,7 +189,7 @@ def nvlink_summary(a, b, steps: int, S: int, N: int, dev):
     set against the algorithmic 2(N-1)/N*S per direction (two-shot / one-shot at N=2)."""
     import torch
     import torch.distributed as dist
-    keys = ("data_tx", "data_rx", "link_tx", "link_rx")
+    keys = ("tx", "rx")
     row = []
     for k in keys:
         ok = isinstance(a, dict) and isinstance(b, dict) and a.get(k) is not None and b.get(k) is not None
@@ -200,9 +200,11 @@ def nvlink_summary(a, b, steps: int, S: int, N: int, dev):
     per_rank = [[None if x < 0 else x for x in r.tolist()] for r in allr]
     alg = 2 * (N - 1) / N * S
     return {"per_rank_per_step": [dict(zip(keys, r)) for r in per_rank],
-            "units": "data_*: NVML THROUGHPUT_DATA (KiB per NVML); link_*: sum of per-link COUNT_*_BYTES",
+            "units": "bytes: nvidia-smi nvlink -gt d (data Tx/Rx, summed over links) per step",
+            "ratio_tx_over_algorithmic": [None if r[0] is None else round(r[0] / alg, 4) for r in per_rank],
+            "ratio_rx_over_algorithmic": [None if r[1] is None else round(r[1] / alg, 4) for r in per_rank],
             "algorithmic_bytes_per_direction_per_step": alg, "steps": steps,
-            "note": "ratio counted/algorithmic needs the unit scale measured by tools/nvlink_counters.py"}
+            "note": "counter scale checked by tools/nvlink_counters.py (peer copy of a known size)"}
 
 
 def _max_over(x: float, dev) -> float:
