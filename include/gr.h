@@ -178,7 +178,9 @@ int gr_mark_ready_async(gr_ctx *ctx, int32_t rank, int32_t tensor_id, void *dev_
  * Errors: GR_ESTATE, GR_ECUDA, GR_ETIMEOUT, GR_EABORT, GR_ESHUTDOWN. */
 int gr_step(gr_ctx *ctx, int32_t *released, gr_cycle_info *info, uint32_t *global_bits);
 
-/* gr_wait — LOCAL. Blocks until every reduction enqueued so far has finished
+/* gr_wait — LOCAL (the end of a step's reduction. PAPER.md:148: a blocking
+ * collective stops the work on the GPU until its result returns — hence gr_wait_async below).
+ * Blocks until every reduction enqueued so far has finished
  * (gradients hold their reduced values) and makes world.compute_stream wait
  * for them. If the step is complete, starts the next step (marks cleared).
  * Errors: GR_ECUDA, GR_ETIMEOUT (a peer stopped mid-reduction). */
@@ -259,8 +261,9 @@ typedef enum {
 } gr_query_kind;
 
 /* GR_ALGO_NVLS: the reduce-scatter runs inside the NVSwitch (multimem.ld_reduce through a
- * multicast mapping, fp32 accumulation) and the result is broadcast with multimem.st; on by
- * default from N = 8 when every GPU supports multicast (environment GR_NVLS=0/1 overrides). */
+ * multicast mapping, fp32 accumulation) and the result is broadcast with multimem.st. Off by
+ * default (it measured slower than two-shot at N = 4 and has not run at N = 8); GR_NVLS=1 at
+ * gr_init enables it when every GPU supports multicast. */
 typedef enum { GR_ALGO_NONE = 0, GR_ALGO_LOCAL = 1, GR_ALGO_ONESHOT = 2, GR_ALGO_TWOSHOT = 3,
                GR_ALGO_NVLS = 4 } gr_algo;
 

@@ -119,12 +119,17 @@ struct DataParams {
     int32_t push;                      // one-/two-shot by TMA bulk stores into peers (1) or by TMA
                                        // bulk loads from peers (0)
     int64_t rsb_stride;                // bytes between receive slots (one fusion buffer)
+    int64_t pub_quantum;               // progress words are published every this many elements of a
+                                       // chunk (and at its end)
     int64_t out_bytes;                 // push: bytes of one shared-memory output tile
     int32_t nout;                      // push: output tiles (2..4) after the stage ring
     char *nvls_uc;                     // NVLS: this rank's copy of the multicast buffer (parity), or null
     char *nvls_mc;                     // NVLS: the multicast view of it (multimem.*), or null
-    uint32_t *pack_flag[GR_MAX_RANKS]; // every rank's pack flags [C][N] for this parity
-    uint32_t *rs_flag[GR_MAX_RANKS];   // every rank's reduce-scatter flags [C] for this parity
+    // progress words (epoch << 32 | e): chunk c's fusion-buffer elements [chunk_begin, e) are done
+    // (packed by source s / reduced by the owner) in this step; published after every stage, so a
+    // consumer of chunk c starts on its first sub-tile instead of waiting for the whole chunk
+    uint64_t *pack_flag[GR_MAX_RANKS]; // every rank's pack progress [C][N] for this parity
+    uint64_t *rs_flag[GR_MAX_RANKS];   // every rank's reduce-scatter progress [C] for this parity
     int32_t *work_counter;             // device, reset by the last CTA
     int32_t *done_counter;
     volatile int32_t *abort_dev;       // device flag: bail out (set on timeout)

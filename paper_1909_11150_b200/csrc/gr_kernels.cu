@@ -753,7 +753,7 @@ __global__ void __launch_bounds__(LC_THREADS, GR_LC_MINB) local_kernel(const __g
 // ---------------------------------------------------------------------------------------
 constexpr int XF_THREADS = 512;
 constexpr int XF_CONS = XF_THREADS - 64;  // warp 0 producer, warp 1 publisher, warps 2.. consumers
-constexpr int XF_PUB = 8;                   // publication ring (chunk flags waiting for the fence)
+constexpr int XF_PUB = 32;                  // publication ring (progress waiting for the fence)
 constexpr int XF_OUT = 4;                   // push: max output tiles (runtime count: p.nout)
 constexpr int XF_PF = 8;                    // push: chunk flags deferred until their bulk stores complete
 constexpr int XF_STAGES = 8;  // max ring depth (runtime depth: p.nstages)
@@ -813,11 +813,27 @@ __device__ __forceinline__ bool mbar_test(uint64_t *b, uint32_t parity) {
     return done != 0;
 }
 
-// thread 0 of the producer: wait until *flag == epoch (or abort / timeout); false = abort
-__device__ __forceinline__ bool xf_wait_flag(const DataParams &p, const uint32_t *flag, int where) {
-    if (ld_acquire_sys(flag) == p.epoch) return true;
+__device__ __forceinline__ uint64_t ld_acquire_sys64(const uint64_t *p) {
+    uint64_t v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+// progress word of this step: epoch in the high half, elements done (absolute fusion-buffer
+// index of the end of the finished prefix of the chunk) in the low half
+__device__ __forceinline__ uint64_t progress_word(uint32_t epoch, int64_t done) {
+    return ((uint64_t)epoch << 32) | (uint64_t)(uint32_t)done;
+}
+// a producer lane: wait until *flag reports this step's progress >= need (or abort / timeout);
+// `known` caches the progress already seen (no re-poll while need <= known). false = abort
+__device__ __forceinline__ bool xf_wait_progress(const DataParams &p, const uint64_t *flag, uint32_t need,
+                                                 uint32_t &known, int where) {
+    uint64_t v = ld_acquire_sys64(flag);
+    if ((uint32_t)(v >> 32) == p.epoch && (uint32_t)v >= need) { known = (uint32_t)v; return true; }
     const uint64_t deadline = globaltimer() + p.timeout_ns;
-    while (ld_acquire_sys(flag) != p.epoch) {
+    for (;;) {
+        __nanosleep(32);
+        v = ld_acquire_sys64(flag);
+        if ((uint32_t)(v >> 32) == p.epoch && (uint32_t)v >= need) { known = (uint32_t)v; return true; }
         if (*p.abort_dev) return false;
         if (globaltimer() > deadline) {
             *p.abort_dev = 1;
@@ -825,9 +841,7 @@ __device__ __forceinline__ bool xf_wait_flag(const DataParams &p, const uint32_t
             p.err->code = ST_TIMEOUT;
             return false;
         }
-        __nanosleep(32);
     }
-    return true;
 }
 
 __device__ __forceinline__ void mbar_expect_tx(uint64_t *b, uint32_t tx) {
@@ -1038,9 +1052,10 @@ __device__ __forceinline__ void xfer_body(const DataParams &p, const int cta, co
     __shared__ __align__(8) uint64_t full[XF_STAGES], empty[XF_STAGES];
     __shared__ __align__(8) uint64_t pub_full[XF_PUB], pub_empty[XF_PUB];
     __shared__ int pub_kind[XF_PUB], pub_chunk[XF_PUB];
+    __shared__ int64_t pub_done[XF_PUB];
     __shared__ __align__(8) uint64_t out_full[XF_OUT], out_empty[XF_OUT];
     __shared__ int out_kind[XF_OUT], out_chunk[XF_OUT], out_last[XF_OUT], out_nb[XF_OUT];
-    __shared__ int64_t out_sb[XF_OUT];
+    __shared__ int64_t out_sb[XF_OUT], out_se[XF_OUT];
     __shared__ XfMeta meta[XF_STAGES];
     __shared__ int s_cum[XF_RCACHE], s_cb[XF_RCACHE];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -1100,8 +1115,15 @@ __device__ __forceinline__ void xfer_body(const DataParams &p, const int cta, co
         long long prof_empty = 0, prof_flags = 0;  // trace mode: producer stall cycles
         const long long prof_t0 = clock64();
         // stream chunk c as sub-tiles of `sub` elements. src: 0 none (PACK), 1 every peer
-        // (RED/RS), 2 the owner (AG); grads: stage own gradient pieces (PACK/RED/RS)
-        auto produce = [&](int kind, int item, int c, int64_t sub, int src, int owner, bool grads) {
+        // (RED/RS), 2 the owner (AG); grads: stage own gradient pieces (PACK/RED/RS).
+        // Dependencies at sub-tile granularity: before sub-tile [sb, se) is staged, every lane q
+        // in wmask waits until progress word wbase[q * wstride] covers se — lane q is the lane
+        // that then issues source q's copy, so its acquire orders that TMA read.
+        // Returns false on abort / timeout.
+        auto produce = [&](int kind, int item, int c, int64_t sub, int src, int owner, bool grads,
+                           const uint64_t *wbase, int wstride, unsigned wmask, int where,
+                           uint64_t *tr) -> bool {
+            uint32_t known = 0;
             const Chunk ch = p.chunks[c];
             const int nseg = ch.seg_end - ch.seg_begin;
             Seg sg{};
@@ -1115,6 +1137,17 @@ __device__ __forceinline__ void xfer_body(const DataParams &p, const int cta, co
             const int nsub = (int)((ce - cb + sub - 1) / sub);
             for (int t = 0; t < nsub; ++t) {
                 const int64_t sb = cb + t * sub, se = (sb + sub < ce) ? sb + sub : ce;
+                if (wmask) {
+                    int ok = 1;
+                    if (((wmask >> lane) & 1u) && known < (uint32_t)se) {
+                        const long long t0 = clock64();
+                        ok = xf_wait_progress(p, wbase + (size_t)lane * wstride, (uint32_t)se, known, where);
+                        prof_flags += clock64() - t0;
+                    }
+                    if (!__all_sync(FULL, ok)) return false;
+                    asm volatile("fence.proxy.async.global;" ::: "memory");  // acquire -> TMA reads
+                    if (t == 0 && tr && lane == 0) tr[1] = globaltimer();
+                }
                 if (lane == 0) {
                     const long long t0 = clock64();
                     mbar_wait(&empty[stage], ph);
@@ -1181,19 +1214,7 @@ __device__ __forceinline__ void xfer_body(const DataParams &p, const int cta, co
                 if (lane == 0) mbar_arrive(bar);  // release: meta + expected bytes registered
                 if (++stage == nst) { stage = 0; ph ^= 1; }
             }
-        };
-        // lane 0: wait for all flags, broadcast the verdict, order the TMA reads after it
-        auto wait_flags = [&](const uint32_t *base, int stride, int count, int skip, int where) -> bool {
-            int ok = 1;
-            if (lane == 0) {
-                const long long t0 = clock64();
-                for (int q = 0; q < count && ok; ++q)
-                    if (q != skip) ok = xf_wait_flag(p, base + (size_t)q * stride, where);
-                prof_flags += clock64() - t0;
-            }
-            ok = __shfl_sync(FULL, ok, 0);
-            asm volatile("fence.proxy.async.global;" ::: "memory");
-            return ok != 0;
+            return true;
         };
         int kq = 0;
         if (lane == 0) kq = atomicAdd(p.work_counter, 1);
@@ -1207,7 +1228,7 @@ __device__ __forceinline__ void xfer_body(const DataParams &p, const int cta, co
                 const int c = chunk_of(k);
                 if (!(ALGO == ALGO_TWOSHOT && c % p.N == p.rank)) {
                     if (p.trace && lane == 0) { const uint64_t t = globaltimer(); p.trace[(size_t)k * 4] = t; p.trace[(size_t)k * 4 + 1] = t; }
-                    produce(K_PACK, k, c, p.sub_pack, 0, -1, true);
+                    produce(K_PACK, k, c, p.sub_pack, 0, -1, true, nullptr, 0, 0u, 0, nullptr);
                 }
             }
             // RED(k-L1) (one-shot, every chunk) / RS(k-L1) (two-shot, owned chunks)
@@ -1217,14 +1238,16 @@ __device__ __forceinline__ void xfer_body(const DataParams &p, const int cta, co
                 if (ALGO == ALGO_ONESHOT || c % p.N == p.rank) {
                     uint64_t *tr = p.trace ? p.trace + ((size_t)total + i1) * 4 : nullptr;
                     if (tr && lane == 0) tr[0] = globaltimer();
-                    // one-shot and NVLS also wait for their own PACK(c) (RED overwrites g after
-                    // PACK read it; the switch reads this rank's copy too)
-                    ok = wait_flags(p.pack_flag[p.rank] + (size_t)c * p.N, 1, p.N, ALGO == ALGO_TWOSHOT ? p.rank : -1, 1);
-                    if (!ok) break;
-                    if (tr && lane == 0) tr[1] = globaltimer();
+                    // every source's pack progress must cover the sub-tile; one-shot and NVLS also
+                    // wait for their own PACK(c) (RED overwrites g after PACK read it; the switch
+                    // reads this rank's copy too)
+                    const uint64_t *wb = p.pack_flag[p.rank] + (size_t)c * p.N;
+                    const unsigned all = (1u << p.N) - 1u;
+                    const unsigned wm = ALGO == ALGO_TWOSHOT ? all & ~(1u << p.rank) : all;
                     // NVLS: no staging, the consumers' own multimem loads are in flight -> whole chunk
-                    if (ALGO == ALGO_NVLS) produce(K_NRS, total + i1, c, 1 << 30, 0, -1, false);
-                    else produce(ALGO == ALGO_ONESHOT ? K_RED : K_RS, total + i1, c, p.sub_red, 1, -1, true);
+                    if (ALGO == ALGO_NVLS) ok = produce(K_NRS, total + i1, c, 1 << 30, 0, -1, false, wb, 1, wm, 1, tr);
+                    else ok = produce(ALGO == ALGO_ONESHOT ? K_RED : K_RS, total + i1, c, p.sub_red, 1, -1, true, wb, 1, wm, 1, tr);
+                    if (!ok) break;
                 }
             }
             // AG(k-L2) (two-shot: pull the owner's reduced chunk; NVLS: it is already in this
@@ -1237,13 +1260,19 @@ __device__ __forceinline__ void xfer_body(const DataParams &p, const int cta, co
                     if (owner != p.rank) {
                         uint64_t *tr = p.trace ? p.trace + ((size_t)2 * total + i2) * 4 : nullptr;
                         if (tr && lane == 0) tr[0] = globaltimer();
-                        ok = wait_flags(p.rs_flag[p.rank] + c, 0, 1, -1, 2);
+                        // the owner's reduce-scatter progress, polled by the lane that issues the copy
+                        ok = produce(K_AG, 2 * total + i2, c, p.sub_ag, ALGO == ALGO_NVLS ? 3 : 2, owner, false,
+                                     p.rs_flag[p.rank] + c, 0, 1u << (ALGO == ALGO_NVLS ? 0 : owner), 2, tr);
                         if (!ok) break;
-                        if (tr && lane == 0) tr[1] = globaltimer();
-                        produce(K_AG, 2 * total + i2, c, p.sub_ag, ALGO == ALGO_NVLS ? 3 : 2, owner, false);
                     }
                 }
             }
+        }
+        // flag waits are spread over the polling lanes: report the largest
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const long long x = __shfl_xor_sync(FULL, prof_flags, o);
+            prof_flags = x > prof_flags ? x : prof_flags;
         }
         if (lane == 0) {  // stop message
             mbar_wait(&empty[stage], ph);
@@ -1263,12 +1292,13 @@ __device__ __forceinline__ void xfer_body(const DataParams &p, const int cta, co
         // peers — the fence latency never stalls the consumer pipeline.
         if (lane == 0 && pushed) {
             // push: issue each finished output tile as TMA bulk stores into the peers (one bulk
-            // group per tile), recycle a tile once its stores have read it, and publish a
-            // chunk's flag only after the stores of its last tile have COMPLETED (deferred: the
-            // flag waits for completion two tiles later, or at once when no tile is ready).
+            // group per tile), recycle a tile once its stores have read it, and publish a tile's
+            // progress only after its stores have COMPLETED (deferred: two tiles later, or at
+            // once when no tile is ready).
             int j = 0, issued = 0;
             uint32_t ph = 0;
             int pf_kind[XF_PF], pf_chunk[XF_PF], pf_group[XF_PF];
+            int64_t pf_done[XF_PF];
             int pf_n = 0;
             const int keep = p.nout - 1;  // groups allowed to still read shared memory
             auto flags = [&](int upto) {  // publish the deferred flags of groups <= upto
@@ -1276,15 +1306,23 @@ __device__ __forceinline__ void xfer_body(const DataParams &p, const int cta, co
                 fence_sys();
                 int k = 0;
                 for (int i = 0; i < pf_n; ++i) {
-                    if (pf_group[i] > upto) { pf_kind[k] = pf_kind[i]; pf_chunk[k] = pf_chunk[i]; pf_group[k] = pf_group[i]; ++k; continue; }
+                    if (pf_group[i] > upto) {
+                        pf_kind[k] = pf_kind[i]; pf_chunk[k] = pf_chunk[i]; pf_group[k] = pf_group[i]; pf_done[k] = pf_done[i];
+                        ++k;
+                        continue;
+                    }
+                    // the next entry of the same chunk (also published now) supersedes this one
+                    if (i + 1 < pf_n && pf_group[i + 1] <= upto && pf_kind[i + 1] == pf_kind[i] && pf_chunk[i + 1] == pf_chunk[i])
+                        continue;
                     const int c = pf_chunk[i];
+                    const uint64_t v = progress_word(p.epoch, pf_done[i]);
                     if (pf_kind[i] == K_RS) {
                         for (int q = 0; q < p.N; ++q)
-                            if (q != p.rank) st_relaxed_sys32(p.rs_flag[q] + c, p.epoch);
+                            if (q != p.rank) st_relaxed_sys64(p.rs_flag[q] + c, v);
                     } else if (ALGO == ALGO_TWOSHOT) {
-                        st_relaxed_sys32(p.pack_flag[c % p.N] + (size_t)c * p.N + p.rank, p.epoch);
+                        st_relaxed_sys64(p.pack_flag[c % p.N] + (size_t)c * p.N + p.rank, v);
                     } else {  // one-shot: every receiver, and this rank (its RED(c) overwrites g after PACK(c) read it)
-                        for (int q = 0; q < p.N; ++q) st_relaxed_sys32(p.pack_flag[q] + (size_t)c * p.N + p.rank, p.epoch);
+                        for (int q = 0; q < p.N; ++q) st_relaxed_sys64(p.pack_flag[q] + (size_t)c * p.N + p.rank, v);
                     }
                 }
                 pf_n = k;
@@ -1313,11 +1351,12 @@ __device__ __forceinline__ void xfer_body(const DataParams &p, const int cta, co
                 }
                 bulk_commit();
                 ++issued;
-                if (out_last[j]) {
+                {   // every tile advances its chunk's progress
                     if (pf_n == XF_PF) { bulk_wait(0); flags(issued - 1); }
                     pf_kind[pf_n] = kind;
                     pf_chunk[pf_n] = c;
                     pf_group[pf_n] = issued;
+                    pf_done[pf_n] = out_se[j];
                     ++pf_n;
                 }
                 // the tile of group issued-keep has been read: hand it back to the consumers
@@ -1333,17 +1372,24 @@ __device__ __forceinline__ void xfer_body(const DataParams &p, const int cta, co
                 mbar_wait(&pub_full[ps], ph);
                 const int kind = pub_kind[ps], c = pub_chunk[ps];
                 if (kind == K_STOP) break;
+                int64_t done = pub_done[ps];
+                // coalesce: later progress of the same chunk already waiting supersedes this one
+                for (;;) {
+                    mbar_arrive(&pub_empty[ps]);
+                    if (++ps == XF_PUB) { ps = 0; ph ^= 1; }
+                    if (!mbar_test(&pub_full[ps], ph) || pub_kind[ps] != kind || pub_chunk[ps] != c) break;
+                    done = pub_done[ps];
+                }
                 fence_sys();
+                const uint64_t v = progress_word(p.epoch, done);
                 if (kind == K_RS || kind == K_NRS) {
                     for (int q = 0; q < p.N; ++q)
-                        if (q != p.rank) st_relaxed_sys32(p.rs_flag[q] + c, p.epoch);
+                        if (q != p.rank) st_relaxed_sys64(p.rs_flag[q] + c, v);
                 } else if (ALGO == ALGO_TWOSHOT || ALGO == ALGO_NVLS) {  // the owner (NVLS: possibly this rank)
-                    st_relaxed_sys32(p.pack_flag[c % p.N] + (size_t)c * p.N + p.rank, p.epoch);
+                    st_relaxed_sys64(p.pack_flag[c % p.N] + (size_t)c * p.N + p.rank, v);
                 } else {  // every rank, this one included: RED(c) must not overwrite g before PACK(c) read it
-                    for (int q = 0; q < p.N; ++q) st_relaxed_sys32(p.pack_flag[q] + (size_t)c * p.N + p.rank, p.epoch);
+                    for (int q = 0; q < p.N; ++q) st_relaxed_sys64(p.pack_flag[q] + (size_t)c * p.N + p.rank, v);
                 }
-                mbar_arrive(&pub_empty[ps]);
-                if (++ps == XF_PUB) { ps = 0; ph ^= 1; }
             }
         }
     } else {
@@ -1354,16 +1400,19 @@ __device__ __forceinline__ void xfer_body(const DataParams &p, const int cta, co
         uint32_t pph = 1;  // publication slots start free
         int ot = 0;
         uint32_t oph = 1;  // output tiles start free
+        int pub_c = -1;    // chunk whose progress was last published, and up to where
+        int64_t pub_at = 0;
         long long prof_full = 0, prof_flag = 0;
         const long long prof_t0 = clock64();
         // hand a finished chunk (or the stop message) to the publisher
-        auto publish = [&](int kind, int c) {
+        auto publish = [&](int kind, int c, int64_t done) {
             const long long t0 = clock64();
             if (lane == 0) mbar_wait(&pub_empty[ps], pph);
             __syncwarp();
             if (ct == 0) {
                 pub_kind[ps] = kind;
                 pub_chunk[ps] = c;
+                pub_done[ps] = done;
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&pub_full[ps]);  // release: this warp's stores, ct 0's meta
@@ -1406,12 +1455,19 @@ __device__ __forceinline__ void xfer_body(const DataParams &p, const int cta, co
                     out_chunk[ot] = c;
                     out_last[ot] = last;
                     out_sb[ot] = msb;
+                    out_se[ot] = mse;
                     out_nb[ot] = (int)(((mse - msb) * B::ES + 15) & ~(int64_t)15);
                 }
                 if (lane == 0) mbar_arrive(&out_full[ot]);  // release: this warp's tile writes, ct 0's meta
                 if (++ot == p.nout) { ot = 0; oph ^= 1; }
-            } else if (last && (kind == K_PACK || kind == K_RS || kind == K_NRS)) {
-                publish(kind, c);
+            } else if (kind == K_PACK || kind == K_RS || kind == K_NRS) {
+                // progress of chunk c: [chunk_begin, mse) done — published at the chunk's end and
+                // every p.pub_quantum elements before it (each publication costs a system fence)
+                if (c != pub_c) { pub_c = c; pub_at = p.chunk_begin[c]; }
+                if (last || mse - pub_at >= p.pub_quantum) {
+                    publish(kind, c, mse);
+                    pub_at = mse;
+                }
             }
             if (p.trace && last && ct == 0) {
                 uint32_t smid;
@@ -1427,7 +1483,7 @@ __device__ __forceinline__ void xfer_body(const DataParams &p, const int cta, co
             if (ct == 0) out_kind[ot] = K_STOP;
             if (lane == 0) mbar_arrive(&out_full[ot]);
         } else {
-            publish(K_STOP, 0);
+            publish(K_STOP, 0, 0);
         }
         if (p.trace && ct == 0) {
             uint64_t *pr = p.trace + (size_t)3 * p.trace_items + (size_t)cta * 8;

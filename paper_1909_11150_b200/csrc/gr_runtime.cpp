@@ -117,7 +117,7 @@ struct gr_ctx {
     cudaEvent_t ring_ev[GR_SLOT_RING] = {};
     bool ring_pending[GR_SLOT_RING] = {};
     char *symm = nullptr;
-    size_t symm_bytes = 0, off_slot = 0, off_pad = 0, off_buf = 0, pad_parity_u32 = 0;
+    size_t symm_bytes = 0, off_slot = 0, off_pad = 0, off_buf = 0, pad_parity_u64 = 0;
     size_t buf_parity_bytes = 0;
     size_t off_rsb = 0, rsb_parity_bytes = 0;  // push two-shot receive slots (N-1 buffers per parity)
     bool push = false;                           // GR_PUSH=1: push two-shot (measured slower)
@@ -161,6 +161,7 @@ struct gr_ctx {
     int lag1 = 0, lag2 = 0;  // GR_LAG1 / GR_LAG2 overrides (tuning)
     int nstages = 4, stage_kb = 48;  // GR_STAGES / GR_STAGE_KB overrides (tuning)
     int nout = 2, out_kb = 24;       // push: output tiles (GR_OUT_TILES / GR_OUT_KB overrides)
+    int64_t pub_quantum = 1ll << 40; // progress publication quantum (elements; GR_PUB_QUANTUM), default: chunk end only
     int64_t lc_sub = 2048;           // local kernel sub-item (GR_LC_SUB, tuning; measured best)
     std::vector<void *> async_streams;  // distinct streams of this step's gr_mark_ready_async calls
 
@@ -332,6 +333,10 @@ int build_layouts(gr_ctx *c, const gr_tensor *table, const int32_t *group_of) {
         c->gelems[g] += c->numel[t];
     }
     c->buf_elems = (off + 7) / 8 * 8;
+    // progress words carry fusion-buffer element indices in 32 bits (gr_kernels.cu)
+    if (c->buf_elems >= (1ll << 32))
+        return fail(nullptr, GR_EINVAL, "%lld gradient elements exceed the 2^32 fusion-buffer index range",
+                    (long long)c->buf_elems);
 
     // chunks: cut each group's range at chunk_elems, segments = tensor pieces
     c->gchunk_begin.assign(G, 0);
@@ -466,12 +471,12 @@ int setup_local(gr_ctx *c) {
     if (c->vg)
         for (int i = 0; i < 2; ++i) CK(c, cudaEventCreateWithFlags(&c->ev_vin[i], cudaEventDisableTiming));
 
-    // symmetric memory: [LL bitvector slots 2 x W u64][flag pad 2 x (C*N + C) u32][fusion buffer 2 x E]
+    // symmetric memory: [LL bitvector slots 2 x W u64][progress pad 2 x (C*N + C) u64][fusion buffer 2 x E]
     const int esz = c->buf_f16 ? 2 : 4;
     c->off_slot = 0;
     c->off_pad = align_up(sizeof(uint64_t) * 2 * (size_t)c->W, kAlign);
-    c->pad_parity_u32 = (size_t)c->C * c->N + c->C;
-    c->off_buf = align_up(c->off_pad + sizeof(uint32_t) * 2 * c->pad_parity_u32, kAlign);
+    c->pad_parity_u64 = (size_t)c->C * c->N + c->C;
+    c->off_buf = align_up(c->off_pad + sizeof(uint64_t) * 2 * c->pad_parity_u64, kAlign);
     c->buf_parity_bytes = (c->N > 1) ? align_up((size_t)c->buf_elems * esz, kAlign) : 0;
     c->off_rsb = c->off_buf + 2 * c->buf_parity_bytes;
     c->rsb_parity_bytes = (c->N > 1 && c->push) ? (size_t)(c->N - 1) * c->buf_parity_bytes : 0;
@@ -543,6 +548,7 @@ int setup_local(gr_ctx *c) {
         if (const char *ok = getenv("GR_OUT_KB")) c->out_kb = std::max(4, atoi(ok) / 4 * 4);
         if (c->nout * c->out_kb > 104) c->out_kb = 104 / c->nout / 4 * 4;
     }
+    if (const char *pq = getenv("GR_PUB_QUANTUM")) c->pub_quantum = std::max<int64_t>(256, atoll(pq));
     if (const char *ns = getenv("GR_STAGES")) c->nstages = std::max(2, std::min(8, atoi(ns)));
     if (const char *sk = getenv("GR_STAGE_KB")) c->stage_kb = std::max(8, atoi(sk));
     const int budget = 208 - (c->push ? c->nout * c->out_kb : 0);
@@ -810,6 +816,10 @@ static int create_ctx(gr_ctx **out, const gr_world *world, const gr_tensor *tabl
     c->chunk_elems = world->chunk_elems;  // 0: adaptive per group (build_layouts)
     if (const char *ls = getenv("GR_LC_SUB")) c->lc_sub = std::max<int64_t>(256, atoll(ls) / 8 * 8);  // tuning
     if (const char *pu = getenv("GR_PUSH")) c->push = atoi(pu) != 0;  // tuning / comparison
+    // adaptive chunk rule: about N x 148 chunks per group (every rank owns ~one reduce-scatter
+    // chunk per SM of each group; measured 64 MiB at N=4: 220 vs 268 us with one per SM,
+    // profiles/r02/sw5_n4_queue_shape.txt), power of two in [8K, 128K] elements
+    c->chunk_target_div = 148 * (int64_t)std::max(1, world->world_size);
     if (const char *cd = getenv("GR_CHUNK_DIV")) c->chunk_target_div = std::max<int64_t>(1, atoll(cd));  // tuning
     if (const char *cm = getenv("GR_CHUNK_MAX")) c->chunk_max = std::max<int64_t>(8192, atoll(cm));      // tuning
     if (world->chunk_elems == 0)
@@ -1198,7 +1208,7 @@ static int step_impl(gr_ctx *c, int32_t *released, gr_cycle_info *info, uint32_t
             char *base = c->peer_symm[r];
             d.buf[r] = base + c->off_buf + (size_t)par * c->buf_parity_bytes;
             d.rsb[r] = c->push ? base + c->off_rsb + (size_t)par * c->rsb_parity_bytes : nullptr;
-            uint32_t *pad = reinterpret_cast<uint32_t *>(base + c->off_pad) + (size_t)par * c->pad_parity_u32;
+            uint64_t *pad = reinterpret_cast<uint64_t *>(base + c->off_pad) + (size_t)par * c->pad_parity_u64;
             d.pack_flag[r] = pad;
             d.rs_flag[r] = pad + (size_t)c->C * c->N;
         }
@@ -1224,6 +1234,7 @@ static int step_impl(gr_ctx *c, int32_t *released, gr_cycle_info *info, uint32_t
         if (c->push) spk = std::min<int64_t>(spk, (int64_t)c->out_kb * 1024 / es / 256 * 256);  // one output tile
         d.sub_pack = std::max<int64_t>(256, std::min<int64_t>(spk, cmax));
         d.out_bytes = (int64_t)c->out_kb * 1024;
+        d.pub_quantum = c->pub_quantum;
         d.nout = c->nout;
         d.sub_ag = std::max<int64_t>(256, std::min<int64_t>(stage / es / 256 * 256, cmax));
         d.one_shot_max_bytes = c->one_shot_max_bytes;

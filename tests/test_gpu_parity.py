@@ -374,9 +374,12 @@ def test_multi_gpu_grad_stats(n):
     assert _torchrun(n, "--suite", "stats", "--seeds", "0:3") == 0
 
 
-def test_autograd_reducer_n1(gpu):
+@pytest.mark.parametrize("set_to_none", [False, True])
+def test_autograd_reducer_n1(gpu, set_to_none):
     """NEXT-3 at N=1: hooks mark the gradients during backward; after synchronize() each
-    gradient equals fl32(fl16(plain-backward gradient)) bit for bit (reading R7-R9 at N=1)."""
+    gradient equals fl32(fl16(plain-backward gradient)) bit for bit (reading R7-R9 at N=1).
+    set_to_none=True is PyTorch's default zero_grad(): every step hands each parameter a NEW
+    gradient buffer, so the reducer must reduce the pointers of that step."""
     import torch
     from harness.fcdensenet import batch, make_model
     from paper_1909_11150_b200.torch_reducer import GroupedGradReducer
@@ -386,7 +389,7 @@ def test_autograd_reducer_n1(gpu):
     red = GroupedGradReducer(model.parameters(), rank=0, world_size=1, device=0, n_groups=3)
     for step in range(3):
         x, y = batch(step, 0, gpu)
-        model.zero_grad(set_to_none=False)
+        model.zero_grad(set_to_none=set_to_none)
         ref.load_state_dict(model.state_dict())
         ref.zero_grad(set_to_none=False)
         torch.nn.functional.mse_loss(model(x), y).backward()
