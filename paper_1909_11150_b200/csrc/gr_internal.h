@@ -106,7 +106,10 @@ enum Algo { ALGO_LOCAL = 1, ALGO_ONESHOT = 2, ALGO_TWOSHOT = 3, ALGO_NVLS = 4 };
 struct DataParams {
     const Seg *segs;
     const Chunk *chunks;
-    const int32_t *group_chunk_begin;  // [G]
+    const int32_t *group_chunk_begin;  // [G] (coarse chunking)
+    const int32_t *group_chunk_begin_fine;  // [G] fine chunking (N > 1; == coarse when there is one)
+    const int32_t *group_nchunks_fine;      // [G]
+    int32_t fine_below;                // messages of fewer coarse chunks than this use the fine chunking
     const int32_t *released;           // ring slot [G]
     const int32_t *cum;                // ring slot [G+1]
     const DevCycle *info;              // ring slot: released groups / chunks / elements
@@ -134,6 +137,8 @@ struct DataParams {
     int32_t *done_counter;
     volatile int32_t *abort_dev;       // device flag: bail out (set on timeout)
     HostError *err;                    // host-mapped
+    uint64_t *dbg;                     // optional [CTAs][4] (GR_DEBUG_DUMP): producer state — triple,
+                                       // kind<<32|chunk, sub-tile<<32|waiting lanes, progress needed
     uint64_t *trace;                   // optional [items][4]: grab, ready, done, cta|smid<<32, then
                                        // per CTA 8 u64 of stall counters (xfer kernel)
     int32_t trace_items;               // item slots in the trace before the per-CTA counters (= C)
@@ -143,7 +148,7 @@ struct DataParams {
     int32_t nstages;                   // xfer kernel: ring depth (<= 8, nstages*stage_bytes <= 208 KB)
     int64_t slot_bytes_red;            // bytes of one peer's slot inside a stage
     int64_t sub_red, sub_ag, sub_pack; // staged sub-tile (elements) for reduce / all-gather / pack items
-    int32_t lag1, lag2;                // queue lags (in released chunks) of reduce / all-gather items
+    int32_t lag1, lag2;                // queue lags (in work items) of reduce / all-gather items
     int64_t lc_sub;                    // local kernel: elements per warp sub-item (multiple of 8)
     int64_t one_shot_max_bytes;        // N>1: messages up to this many buffer bytes go one-shot
     double *sumsq;                     // optional [T]: sum of squares of the reduced gradient (NEXT-2)

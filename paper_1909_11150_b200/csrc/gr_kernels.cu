@@ -861,7 +861,7 @@ struct Piece {
 
 constexpr int XF_MAXP = 8;  // gradient pieces described in a stage's metadata (more: slow path)
 struct XfMeta {
-    int kind, item, chunk, last;
+    int kind, item, chunk, last, owner;
     int npieces;              // -1: too many pieces, consumers walk the segments themselves
     int64_t sb, se;           // staged fusion-buffer range
     Piece pc[XF_MAXP];
@@ -1051,13 +1051,13 @@ __device__ __forceinline__ void xfer_body(const DataParams &p, const int cta, co
     extern __shared__ __align__(1024) char xsm[];
     __shared__ __align__(8) uint64_t full[XF_STAGES], empty[XF_STAGES];
     __shared__ __align__(8) uint64_t pub_full[XF_PUB], pub_empty[XF_PUB];
-    __shared__ int pub_kind[XF_PUB], pub_chunk[XF_PUB];
+    __shared__ int pub_kind[XF_PUB], pub_chunk[XF_PUB], pub_owner[XF_PUB];
     __shared__ int64_t pub_done[XF_PUB];
     __shared__ __align__(8) uint64_t out_full[XF_OUT], out_empty[XF_OUT];
-    __shared__ int out_kind[XF_OUT], out_chunk[XF_OUT], out_last[XF_OUT], out_nb[XF_OUT];
+    __shared__ int out_kind[XF_OUT], out_chunk[XF_OUT], out_last[XF_OUT], out_nb[XF_OUT], out_owner[XF_OUT];
     __shared__ int64_t out_sb[XF_OUT], out_se[XF_OUT];
     __shared__ XfMeta meta[XF_STAGES];
-    __shared__ int s_cum[XF_RCACHE], s_cb[XF_RCACHE];
+    __shared__ int s_cum[XF_RCACHE], s_cb[XF_RCACHE], s_nch[XF_RCACHE], s_icum[1];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int64_t stage_bytes = p.stage_bytes;
     const int64_t gslot_off = p.slot_bytes_red * (p.N - 1);  // gradient slot inside a RED/RS stage
@@ -1084,12 +1084,29 @@ __device__ __forceinline__ void xfer_body(const DataParams &p, const int cta, co
     const int ALGO = (p.info->elems * B::ES <= p.one_shot_max_bytes) ? ALGO_ONESHOT
                      : (p.nvls_mc ? ALGO_NVLS : ALGO_TWOSHOT);
     const bool cached = nrel <= XF_RCACHE;
+    // chunking of this message: the coarse one (the bitvector kernel's prefix, p.cum) when the
+    // message holds many coarse chunks, else the fine one (every rank then owns about one
+    // reduce-scatter chunk per SM even for a single released group). The decision and the
+    // chunk list follow from the released set, so every rank makes the same.
+    const bool fine = cached && p.group_chunk_begin_fine && total < p.fine_below;
     if (cached)
         for (int j = tid; j < nrel; j += blockDim.x) {
-            s_cum[j] = p.cum[j];
-            s_cb[j] = p.group_chunk_begin[p.released[j]];
+            const int g = p.released[j];
+            s_cb[j] = fine ? p.group_chunk_begin_fine[g] : p.group_chunk_begin[g];
+            s_nch[j] = fine ? p.group_nchunks_fine[g] : p.cum[j + 1] - p.cum[j];
         }
     __syncthreads();
+    if (cached && tid == 0) {
+        int acc = 0;
+        for (int j = 0; j < nrel; ++j) {
+            s_cum[j] = acc;
+            acc += s_nch[j];
+        }
+        s_icum[0] = acc;
+    }
+    __syncthreads();
+    const int titems = cached ? s_icum[0] : total;  // work items (chunks) of this message
+    // item i -> its chunk (the item's position in the message also fixes its owner, i mod N)
     auto chunk_of = [&](int i) -> int {
         if (!cached) return chunk_of_item(p, nrel, i);
         int lo = 0, hi = nrel - 1;
@@ -1099,12 +1116,13 @@ __device__ __forceinline__ void xfer_body(const DataParams &p, const int cta, co
         }
         return s_cb[lo] + (i - s_cum[lo]);
     };
+    const int tstride = p.trace_items / 4;  // trace: item slots per phase
     const int lag1 = p.lag1, lag2 = (ALGO == ALGO_ONESHOT) ? p.lag1 : p.lag2;
     // push (one-/two-shot): packed and reduced sub-tiles leave through shared-memory output tiles
     // that the publisher bulk-stores into the peers (NVLS keeps its multicast path)
     const bool pushed = p.push && ALGO != ALGO_NVLS;
     char *const out_base = xsm + (size_t)nst * stage_bytes;
-    const int nk = total > 0 ? total + lag2 : 0;  // queue triples
+    const int nk = titems > 0 ? titems + lag2 : 0;  // queue triples
     if (warp == 0) {
         // ---------------- producer warp: lane 0 owns the queue, barriers and flag waits;
         // the 32 lanes describe / stage the chunk's gradient pieces and issue the peer
@@ -1122,7 +1140,7 @@ __device__ __forceinline__ void xfer_body(const DataParams &p, const int cta, co
         // Returns false on abort / timeout.
         auto produce = [&](int kind, int item, int c, int64_t sub, int src, int owner, bool grads,
                            const uint64_t *wbase, int wstride, unsigned wmask, int where,
-                           uint64_t *tr) -> bool {
+                           uint64_t *tr, int iowner) -> bool {
             uint32_t known = 0;
             const Chunk ch = p.chunks[c];
             const int nseg = ch.seg_end - ch.seg_begin;
@@ -1139,6 +1157,12 @@ __device__ __forceinline__ void xfer_body(const DataParams &p, const int cta, co
                 const int64_t sb = cb + t * sub, se = (sb + sub < ce) ? sb + sub : ce;
                 if (wmask) {
                     int ok = 1;
+                    if (p.dbg && lane == 0) {  // hang diagnosis: what this CTA waits for
+                        uint64_t *d = p.dbg + (size_t)cta * 8;
+                        d[1] = ((uint64_t)kind << 32) | (uint32_t)c;
+                        d[2] = ((uint64_t)t << 32) | wmask;
+                        d[3] = (uint64_t)se;
+                    }
                     if (((wmask >> lane) & 1u) && known < (uint32_t)se) {
                         const long long t0 = clock64();
                         ok = xf_wait_progress(p, wbase + (size_t)lane * wstride, (uint32_t)se, known, where);
@@ -1184,6 +1208,7 @@ __device__ __forceinline__ void xfer_body(const DataParams &p, const int cta, co
                     m.kind = kind;
                     m.item = item;
                     m.chunk = c;
+                    m.owner = iowner;
                     m.last = t == nsub - 1;
                     m.sb = sb;
                     m.se = se;
@@ -1222,47 +1247,50 @@ __device__ __forceinline__ void xfer_body(const DataParams &p, const int cta, co
         for (;;) {
             const int k = __shfl_sync(FULL, kq, 0);
             if (k >= nk || !ok) break;
+            if (p.dbg && lane == 0) p.dbg[(size_t)cta * 8] = (uint64_t)k;
             if (lane == 0) kq = atomicAdd(p.work_counter, 1);  // prefetch the next triple
-            // PACK(k): own gradients (TMA) -> fusion buffer (consumers), flag -> peers
-            if (k < total) {
+            // PACK(k): own gradients (TMA) -> fusion buffer (consumers), progress -> owner
+            if (k < titems) {
                 const int c = chunk_of(k);
-                if (!(ALGO == ALGO_TWOSHOT && c % p.N == p.rank)) {
+                const int own = k % p.N;
+                if (!(ALGO == ALGO_TWOSHOT && own == p.rank)) {
                     if (p.trace && lane == 0) { const uint64_t t = globaltimer(); p.trace[(size_t)k * 4] = t; p.trace[(size_t)k * 4 + 1] = t; }
-                    produce(K_PACK, k, c, p.sub_pack, 0, -1, true, nullptr, 0, 0u, 0, nullptr);
+                    produce(K_PACK, k, c, p.sub_pack, 0, -1, true, nullptr, 0, 0u, 0, nullptr, own);
                 }
             }
-            // RED(k-L1) (one-shot, every chunk) / RS(k-L1) (two-shot, owned chunks)
+            // RED(k-L1) (one-shot, every item) / RS(k-L1) (two-shot, owned items)
             const int i1 = k - lag1;
-            if (i1 >= 0 && i1 < total) {
+            if (i1 >= 0 && i1 < titems) {
                 const int c = chunk_of(i1);
-                if (ALGO == ALGO_ONESHOT || c % p.N == p.rank) {
-                    uint64_t *tr = p.trace ? p.trace + ((size_t)total + i1) * 4 : nullptr;
+                const int own = i1 % p.N;
+                if (ALGO == ALGO_ONESHOT || own == p.rank) {
+                    uint64_t *tr = p.trace ? p.trace + ((size_t)tstride + i1) * 4 : nullptr;
                     if (tr && lane == 0) tr[0] = globaltimer();
                     // every source's pack progress must cover the sub-tile; one-shot and NVLS also
                     // wait for their own PACK(c) (RED overwrites g after PACK read it; the switch
                     // reads this rank's copy too)
-                    const uint64_t *wb = p.pack_flag[p.rank] + (size_t)c * p.N;
                     const unsigned all = (1u << p.N) - 1u;
                     const unsigned wm = ALGO == ALGO_TWOSHOT ? all & ~(1u << p.rank) : all;
+                    const uint64_t *wb = p.pack_flag[p.rank] + (size_t)c * p.N;
                     // NVLS: no staging, the consumers' own multimem loads are in flight -> whole chunk
-                    if (ALGO == ALGO_NVLS) ok = produce(K_NRS, total + i1, c, 1 << 30, 0, -1, false, wb, 1, wm, 1, tr);
-                    else ok = produce(ALGO == ALGO_ONESHOT ? K_RED : K_RS, total + i1, c, p.sub_red, 1, -1, true, wb, 1, wm, 1, tr);
+                    if (ALGO == ALGO_NVLS) ok = produce(K_NRS, tstride + i1, c, 1 << 30, 0, -1, false, wb, 1, wm, 1, tr, own);
+                    else ok = produce(ALGO == ALGO_ONESHOT ? K_RED : K_RS, tstride + i1, c, p.sub_red, 1, -1, true, wb, 1, wm, 1, tr, own);
                     if (!ok) break;
                 }
             }
-            // AG(k-L2) (two-shot: pull the owner's reduced chunk; NVLS: it is already in this
+            // AG(k-L2) (two-shot: pull the owner's reduced chunks; NVLS: they are already in this
             // rank's copy, written by the owner's multicast store)
             if (ALGO != ALGO_ONESHOT) {
                 const int i2 = k - lag2;
-                if (i2 >= 0 && i2 < total) {
+                if (i2 >= 0 && i2 < titems) {
                     const int c = chunk_of(i2);
-                    const int owner = c % p.N;
+                    const int owner = i2 % p.N;
                     if (owner != p.rank) {
-                        uint64_t *tr = p.trace ? p.trace + ((size_t)2 * total + i2) * 4 : nullptr;
+                        uint64_t *tr = p.trace ? p.trace + ((size_t)2 * tstride + i2) * 4 : nullptr;
                         if (tr && lane == 0) tr[0] = globaltimer();
                         // the owner's reduce-scatter progress, polled by the lane that issues the copy
-                        ok = produce(K_AG, 2 * total + i2, c, p.sub_ag, ALGO == ALGO_NVLS ? 3 : 2, owner, false,
-                                     p.rs_flag[p.rank] + c, 0, 1u << (ALGO == ALGO_NVLS ? 0 : owner), 2, tr);
+                        ok = produce(K_AG, 2 * tstride + i2, c, p.sub_ag, ALGO == ALGO_NVLS ? 3 : 2, owner, false,
+                                     p.rs_flag[p.rank] + c, 0, 1u << (ALGO == ALGO_NVLS ? 0 : owner), 2, tr, owner);
                         if (!ok) break;
                     }
                 }
@@ -1297,7 +1325,7 @@ __device__ __forceinline__ void xfer_body(const DataParams &p, const int cta, co
             // once when no tile is ready).
             int j = 0, issued = 0;
             uint32_t ph = 0;
-            int pf_kind[XF_PF], pf_chunk[XF_PF], pf_group[XF_PF];
+            int pf_kind[XF_PF], pf_chunk[XF_PF], pf_group[XF_PF], pf_owner[XF_PF];
             int64_t pf_done[XF_PF];
             int pf_n = 0;
             const int keep = p.nout - 1;  // groups allowed to still read shared memory
@@ -1308,6 +1336,7 @@ __device__ __forceinline__ void xfer_body(const DataParams &p, const int cta, co
                 for (int i = 0; i < pf_n; ++i) {
                     if (pf_group[i] > upto) {
                         pf_kind[k] = pf_kind[i]; pf_chunk[k] = pf_chunk[i]; pf_group[k] = pf_group[i]; pf_done[k] = pf_done[i];
+                        pf_owner[k] = pf_owner[i];
                         ++k;
                         continue;
                     }
@@ -1320,7 +1349,7 @@ __device__ __forceinline__ void xfer_body(const DataParams &p, const int cta, co
                         for (int q = 0; q < p.N; ++q)
                             if (q != p.rank) st_relaxed_sys64(p.rs_flag[q] + c, v);
                     } else if (ALGO == ALGO_TWOSHOT) {
-                        st_relaxed_sys64(p.pack_flag[c % p.N] + (size_t)c * p.N + p.rank, v);
+                        st_relaxed_sys64(p.pack_flag[pf_owner[i]] + (size_t)c * p.N + p.rank, v);
                     } else {  // one-shot: every receiver, and this rank (its RED(c) overwrites g after PACK(c) read it)
                         for (int q = 0; q < p.N; ++q) st_relaxed_sys64(p.pack_flag[q] + (size_t)c * p.N + p.rank, v);
                     }
@@ -1339,7 +1368,7 @@ __device__ __forceinline__ void xfer_body(const DataParams &p, const int cta, co
                 const uint32_t nb = (uint32_t)out_nb[j];
                 const char *tile = out_base + (size_t)j * p.out_bytes;
                 if (kind == K_PACK && ALGO == ALGO_TWOSHOT) {  // into the owner's receive slot
-                    const int o = c % p.N;
+                    const int o = out_owner[j];
                     bulk_s2g(p.rsb[o] + (size_t)(p.rank < o ? p.rank : p.rank - 1) * p.rsb_stride + sb * B::ES, tile, nb);
                 } else {
                     for (int q = 0; q < p.N; ++q) {
@@ -1357,6 +1386,7 @@ __device__ __forceinline__ void xfer_body(const DataParams &p, const int cta, co
                     pf_chunk[pf_n] = c;
                     pf_group[pf_n] = issued;
                     pf_done[pf_n] = out_se[j];
+                    pf_owner[pf_n] = out_owner[j];
                     ++pf_n;
                 }
                 // the tile of group issued-keep has been read: hand it back to the consumers
@@ -1370,7 +1400,7 @@ __device__ __forceinline__ void xfer_body(const DataParams &p, const int cta, co
         } else if (lane == 0) {
             for (int ps = 0, ph = 0;; ) {
                 mbar_wait(&pub_full[ps], ph);
-                const int kind = pub_kind[ps], c = pub_chunk[ps];
+                const int kind = pub_kind[ps], c = pub_chunk[ps], own = pub_owner[ps];
                 if (kind == K_STOP) break;
                 int64_t done = pub_done[ps];
                 // coalesce: later progress of the same chunk already waiting supersedes this one
@@ -1382,11 +1412,15 @@ __device__ __forceinline__ void xfer_body(const DataParams &p, const int cta, co
                 }
                 fence_sys();
                 const uint64_t v = progress_word(p.epoch, done);
+                if (p.dbg) {
+                    p.dbg[(size_t)cta * 8 + 6] += 1;
+                    p.dbg[(size_t)cta * 8 + 7] = ((uint64_t)kind << 48) | ((uint64_t)(uint32_t)c << 16) | (uint32_t)own;
+                }
                 if (kind == K_RS || kind == K_NRS) {
                     for (int q = 0; q < p.N; ++q)
                         if (q != p.rank) st_relaxed_sys64(p.rs_flag[q] + c, v);
                 } else if (ALGO == ALGO_TWOSHOT || ALGO == ALGO_NVLS) {  // the owner (NVLS: possibly this rank)
-                    st_relaxed_sys64(p.pack_flag[c % p.N] + (size_t)c * p.N + p.rank, v);
+                    st_relaxed_sys64(p.pack_flag[own] + (size_t)c * p.N + p.rank, v);
                 } else {  // every rank, this one included: RED(c) must not overwrite g before PACK(c) read it
                     for (int q = 0; q < p.N; ++q) st_relaxed_sys64(p.pack_flag[q] + (size_t)c * p.N + p.rank, v);
                 }
@@ -1405,7 +1439,7 @@ __device__ __forceinline__ void xfer_body(const DataParams &p, const int cta, co
         long long prof_full = 0, prof_flag = 0;
         const long long prof_t0 = clock64();
         // hand a finished chunk (or the stop message) to the publisher
-        auto publish = [&](int kind, int c, int64_t done) {
+        auto publish = [&](int kind, int c, int64_t done, int own) {
             const long long t0 = clock64();
             if (lane == 0) mbar_wait(&pub_empty[ps], pph);
             __syncwarp();
@@ -1413,6 +1447,7 @@ __device__ __forceinline__ void xfer_body(const DataParams &p, const int cta, co
                 pub_kind[ps] = kind;
                 pub_chunk[ps] = c;
                 pub_done[ps] = done;
+                pub_owner[ps] = own;
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&pub_full[ps]);  // release: this warp's stores, ct 0's meta
@@ -1428,7 +1463,7 @@ __device__ __forceinline__ void xfer_body(const DataParams &p, const int cta, co
             const XfMeta &m = meta[stage];
             const int kind = m.kind;
             if (kind == K_STOP) break;
-            const int item = m.item, c = m.chunk, last = m.last;
+            const int item = m.item, c = m.chunk, last = m.last, mown = m.owner;
             const int64_t msb = m.sb, mse = m.se;
             const char *st = xsm + (size_t)stage * stage_bytes;
             char *own = ALGO == ALGO_NVLS ? p.nvls_uc : p.buf[p.rank];  // this rank's fusion buffer
@@ -1455,6 +1490,7 @@ __device__ __forceinline__ void xfer_body(const DataParams &p, const int cta, co
                     out_chunk[ot] = c;
                     out_last[ot] = last;
                     out_sb[ot] = msb;
+                    out_owner[ot] = mown;
                     out_se[ot] = mse;
                     out_nb[ot] = (int)(((mse - msb) * B::ES + 15) & ~(int64_t)15);
                 }
@@ -1465,9 +1501,13 @@ __device__ __forceinline__ void xfer_body(const DataParams &p, const int cta, co
                 // every p.pub_quantum elements before it (each publication costs a system fence)
                 if (c != pub_c) { pub_c = c; pub_at = p.chunk_begin[c]; }
                 if (last || mse - pub_at >= p.pub_quantum) {
-                    publish(kind, c, mse);
+                    publish(kind, c, mse, mown);
                     pub_at = mse;
                 }
+            }
+            if (p.dbg && ct == 0) {
+                p.dbg[(size_t)cta * 8 + 4] += 1;
+                p.dbg[(size_t)cta * 8 + 5] = ((uint64_t)kind << 48) | ((uint64_t)(uint32_t)c << 16) | (uint32_t)last;
             }
             if (p.trace && last && ct == 0) {
                 uint32_t smid;
@@ -1483,7 +1523,7 @@ __device__ __forceinline__ void xfer_body(const DataParams &p, const int cta, co
             if (ct == 0) out_kind[ot] = K_STOP;
             if (lane == 0) mbar_arrive(&out_full[ot]);
         } else {
-            publish(K_STOP, 0, 0);
+            publish(K_STOP, 0, 0, 0);
         }
         if (p.trace && ct == 0) {
             uint64_t *pr = p.trace + (size_t)3 * p.trace_items + (size_t)cta * 8;

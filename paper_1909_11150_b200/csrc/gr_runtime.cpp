@@ -90,6 +90,7 @@ struct gr_ctx {
     int buf_f16 = 1;
     int64_t chunk_elems = 0;  // 0 = adaptive per group
     int64_t chunk_target_div = 148, chunk_max = 131072;  // adaptive rule (GR_CHUNK_DIV / GR_CHUNK_MAX)
+    int64_t chunk_target_div_fine = 148;                  // fine chunking (N x 148; GR_CHUNK_DIV_FINE)
     int64_t one_shot_max_bytes = 0;
     uint64_t hash = 0;
 
@@ -97,6 +98,10 @@ struct gr_ctx {
     std::vector<int64_t> numel;
     std::vector<int32_t> grad_f16, group_of, bit_of, tensor_of_bit, group_of_bit;
     std::vector<int32_t> gbit_begin, gbit_end, gnchunks, gchunk_begin, gnsub, gspc;
+    // N > 1: a second, finer chunking of every group (about N x 148 chunks per group), appended
+    // after the coarse one; the data kernel takes it for messages with few coarse chunks
+    std::vector<int32_t> gnchunks_f, gchunk_begin_f;
+    int32_t C_coarse = 0;
     std::vector<int64_t> buf_off, gelems;
     std::vector<int32_t> big_groups;
     std::vector<Seg> segs;
@@ -127,6 +132,7 @@ struct gr_ctx {
     int64_t *d_cbeg = nullptr, *d_cend = nullptr;
     gr::GroupInfo *d_groups = nullptr;
     bool stage_groups = false;  // the group records fit the bitvector kernel's shared memory
+    int32_t *d_gcb_f = nullptr, *d_gnc_f = nullptr;
     int32_t *d_gcb = nullptr,
             *d_gspc = nullptr, *d_subcum_ring = nullptr;
     int32_t *d_big = nullptr;
@@ -135,6 +141,8 @@ struct gr_ctx {
     int32_t *d_rel_ring = nullptr, *d_cum_ring = nullptr;
     gr::DevCycle *d_info_ring = nullptr;
     int32_t *d_counters = nullptr;  // [0] work, [1] done, [2] abort
+    uint64_t *d_dbg = nullptr;      // GR_DEBUG_DUMP: per-CTA producer state of the data kernel
+    std::string dbg_path;
     // pinned host-mapped
     uint32_t *h_bits = nullptr;   // sync marks, by bit (live: gr_mark_ready writes, under mu)
     uint32_t *h_marked = nullptr; // every mark (host or stream-ordered), by bit (live, under mu)
@@ -158,10 +166,14 @@ struct gr_ctx {
     PFN_writeValue32 write_value32 = nullptr;
     int data_ctas[4] = {0, 0, 0, 0};       // world.comm_ctas (or every SM)
     int data_ctas_full[4] = {0, 0, 0, 0};  // every SM (drain cycles)
-    int lag1 = 0, lag2 = 0;  // GR_LAG1 / GR_LAG2 overrides (tuning)
-    int nstages = 4, stage_kb = 48;  // GR_STAGES / GR_STAGE_KB overrides (tuning)
+    int lag1 = -1, lag2 = -1;  // GR_LAG1 / GR_LAG2 overrides (tuning; -1 = default multiple of the grid)
+    // TMA stage ring of the xfer kernel: 2 x 96 KB (measured against 4 x 48 / 3 x 64 / 6 x 32 /
+    // 8 x 24 KB: per-stage fixed costs make small stages slow — 0.88 vs 0.81 of HBM peak on
+    // virtual ranks, 2-5% at N = 2/4, profiles/r02/virtual_chunk_stage_sweep.txt)
+    int nstages = 2, stage_kb = 96;  // GR_STAGES / GR_STAGE_KB overrides (tuning)
     int nout = 2, out_kb = 24;       // push: output tiles (GR_OUT_TILES / GR_OUT_KB overrides)
     int64_t pub_quantum = 1ll << 40; // progress publication quantum (elements; GR_PUB_QUANTUM), default: chunk end only
+    int32_t fine_below = -1;         // fine chunking below this many coarse chunks (GR_FINE_BELOW; -1: 2 x N x grid)
     int64_t lc_sub = 2048;           // local kernel sub-item (GR_LC_SUB, tuning; measured best)
     std::vector<void *> async_streams;  // distinct streams of this step's gr_mark_ready_async calls
 
@@ -236,8 +248,33 @@ int fail(gr_ctx *c, int code, const char *fmt, ...) {
 
 // an error reported by a kernel through the pinned error block (data-kernel timeout, or a
 // drain cycle that failed / left the step incomplete)
+// GR_DEBUG_DUMP: on a data-kernel timeout, write every CTA's producer state and this rank's
+// progress pad (both parities) to <prefix>.rank<r>.json (the kernel bailed out; reads are safe)
+void debug_dump(gr_ctx *c) {
+    if (!c->d_dbg || c->dbg_path.empty()) return;
+    std::vector<uint64_t> st(8 * 1024), pad(2 * c->pad_parity_u64);
+    if (cudaMemcpy(st.data(), c->d_dbg, sizeof(uint64_t) * st.size(), cudaMemcpyDeviceToHost) != cudaSuccess) return;
+    if (cudaMemcpy(pad.data(), c->symm + c->off_pad, sizeof(uint64_t) * pad.size(), cudaMemcpyDeviceToHost) != cudaSuccess)
+        return;
+    std::ofstream f(c->dbg_path);
+    f << "{\"rank\":" << c->rank << ",\"N\":" << c->N << ",\"C\":" << c->C << ",\"epoch\":" << c->epoch
+      << ",\"ctas\":[";
+    bool first = true;
+    const int nct = std::min(1024, c->data_ctas_full[gr::ALGO_TWOSHOT]);
+    for (int i = 0; i < nct; ++i) {
+        f << (first ? "" : ",") << "[" << i;
+        for (int j = 0; j < 8; ++j) f << "," << st[8 * i + j];
+        f << "]";
+        first = false;
+    }
+    f << "],\"pad\":[";
+    for (size_t i = 0; i < pad.size(); ++i) f << (i ? "," : "") << pad[i];
+    f << "]}\n";
+}
+
 int device_error(gr_ctx *c) {
     const int code = c->h_err->code, where = c->h_err->where;
+    if (code == 3) debug_dump(c);
     if (code == 3)
         return fail(c, GR_ETIMEOUT, "reduction timed out waiting for a peer (%s flag)", where == 1 ? "pack" : "reduce-scatter");
     if (code >= 10) {
@@ -338,50 +375,66 @@ int build_layouts(gr_ctx *c, const gr_tensor *table, const int32_t *group_of) {
         return fail(nullptr, GR_EINVAL, "%lld gradient elements exceed the 2^32 fusion-buffer index range",
                     (long long)c->buf_elems);
 
-    // chunks: cut each group's range at chunk_elems, segments = tensor pieces
+    // chunks: cut each group's range at chunk_elems, segments = tensor pieces. Pass 0: the
+    // coarse chunking (about one chunk per SM per group, power of two in [8K, 128K] elements:
+    // large items, few flags — best when a message holds many chunks, e.g. all of fcn220m).
+    // Pass 1 (N > 1, adaptive rule): about N x 148 chunks per group, so a group released alone
+    // still gives every rank about one owned reduce-scatter chunk per SM (64 MiB at N=4: 218 vs
+    // 268 us, profiles/r02/sw5_n4_queue_shape.txt); the data kernel picks per message.
     c->gchunk_begin.assign(G, 0);
     c->gnchunks.assign(G, 0);
+    c->gchunk_begin_f.assign(G, 0);
+    c->gnchunks_f.assign(G, 0);
     c->segs.clear();
     c->chunks.clear();
     c->chunk_begin.clear();
     c->chunk_end.clear();
-    int32_t pos = 0;
-    for (int32_t g = 0; g < G; ++g) {
-        c->gchunk_begin[g] = (int32_t)c->chunks.size();
-        const int32_t pos0 = pos;
-        while (pos < T && group_of[order[pos]] == g) ++pos;
-        // chunk size: fixed when the caller asks for one; otherwise per group, about one chunk
-        // per SM for the group alone (power of two in [8K, 128K] elements): large groups get
-        // large items (fewer flags, longer TMA streams), small ones keep every SM busy
-        int64_t cg = c->chunk_elems;
-        if (cg == 0) {
-            const int64_t target = std::max<int64_t>(1, (gend[g] - gbeg[g]) / c->chunk_target_div);
-            cg = 8192;
-            while (cg * 2 <= target && cg < c->chunk_max) cg *= 2;
-        }
-        for (int64_t cb = gbeg[g]; cb < gend[g]; cb += cg) {
-            const int64_t ce = std::min(gend[g], cb + cg);
-            Chunk ch;
-            ch.seg_begin = (int32_t)c->segs.size();
-            for (int32_t q = pos0; q < pos; ++q) {
-                const int32_t t = order[q];
-                const int64_t tb = c->buf_off[t], te = tb + c->numel[t];
-                const int64_t lo = std::max(tb, cb), hi = std::min(te, ce);
-                if (lo >= hi) continue;
-                Seg s;
-                s.tensor = t;
-                s.grad_f16 = c->grad_f16[t];
-                s.tensor_off = lo - tb;
-                s.buf_off = lo;
-                s.len = hi - lo;
-                c->segs.push_back(s);
+    const int passes = (c->N > 1 && c->chunk_elems == 0) ? 2 : 1;
+    for (int pass = 0; pass < passes; ++pass) {
+        std::vector<int32_t> &gcb = pass ? c->gchunk_begin_f : c->gchunk_begin;
+        std::vector<int32_t> &gnc = pass ? c->gnchunks_f : c->gnchunks;
+        const int64_t div = pass ? c->chunk_target_div_fine : c->chunk_target_div;
+        int32_t pos = 0;
+        for (int32_t g = 0; g < G; ++g) {
+            gcb[g] = (int32_t)c->chunks.size();
+            const int32_t pos0 = pos;
+            while (pos < T && group_of[order[pos]] == g) ++pos;
+            int64_t cg = c->chunk_elems;
+            if (cg == 0) {
+                const int64_t target = std::max<int64_t>(1, (gend[g] - gbeg[g]) / div);
+                // fine chunks stay >= 16K elements: 8K ones lost at 8-16 MiB (N = 2 / 4)
+                cg = pass ? 16384 : 8192;
+                while (cg * 2 <= target && cg < c->chunk_max) cg *= 2;
             }
-            ch.seg_end = (int32_t)c->segs.size();
-            c->chunks.push_back(ch);
-            c->chunk_begin.push_back(cb);
-            c->chunk_end.push_back(ce);
+            for (int64_t cb = gbeg[g]; cb < gend[g]; cb += cg) {
+                const int64_t ce = std::min(gend[g], cb + cg);
+                Chunk ch;
+                ch.seg_begin = (int32_t)c->segs.size();
+                for (int32_t q = pos0; q < pos; ++q) {
+                    const int32_t t = order[q];
+                    const int64_t tb = c->buf_off[t], te = tb + c->numel[t];
+                    const int64_t lo = std::max(tb, cb), hi = std::min(te, ce);
+                    if (lo >= hi) continue;
+                    Seg sgm;
+                    sgm.tensor = t;
+                    sgm.grad_f16 = c->grad_f16[t];
+                    sgm.tensor_off = lo - tb;
+                    sgm.buf_off = lo;
+                    sgm.len = hi - lo;
+                    c->segs.push_back(sgm);
+                }
+                ch.seg_end = (int32_t)c->segs.size();
+                c->chunks.push_back(ch);
+                c->chunk_begin.push_back(cb);
+                c->chunk_end.push_back(ce);
+            }
+            gnc[g] = (int32_t)c->chunks.size() - gcb[g];
         }
-        c->gnchunks[g] = (int32_t)c->chunks.size() - c->gchunk_begin[g];
+        if (pass == 0) c->C_coarse = (int32_t)c->chunks.size();
+    }
+    if (passes == 1) {  // one chunking: the "fine" tables are the coarse ones
+        c->gchunk_begin_f = c->gchunk_begin;
+        c->gnchunks_f = c->gnchunks;
     }
     c->C = (int32_t)c->chunks.size();
     // local-kernel sub-items (N = 1): lc_sub elements each, spc per full chunk of a group
@@ -409,8 +462,10 @@ int build_layouts(gr_ctx *c, const gr_tensor *table, const int32_t *group_of) {
     h = fnv1a(h, &c->push, sizeof c->push);
     h = fnv1a(h, &c->lag1, sizeof c->lag1);
     h = fnv1a(h, &c->lag2, sizeof c->lag2);
+    h = fnv1a(h, &c->fine_below, sizeof c->fine_below);
     h = fnv1a(h, &c->world.comm_ctas, sizeof c->world.comm_ctas);  // sets the default lags (x grid)
     h = fnv1a(h, &c->chunk_target_div, sizeof c->chunk_target_div);
+    h = fnv1a(h, &c->chunk_target_div_fine, sizeof c->chunk_target_div_fine);
     h = fnv1a(h, &c->chunk_max, sizeof c->chunk_max);
     h = fnv1a(h, c->numel.data(), sizeof(int64_t) * T);
     h = fnv1a(h, c->grad_f16.data(), sizeof(int32_t) * T);
@@ -496,6 +551,8 @@ int setup_local(gr_ctx *c) {
         RC(upload(c, &c->d_groups, gi));
     }
     RC(upload(c, &c->d_gcb, c->gchunk_begin));
+    RC(upload(c, &c->d_gcb_f, c->gchunk_begin_f));
+    RC(upload(c, &c->d_gnc_f, c->gnchunks_f));
     RC(upload(c, &c->d_gspc, c->gspc));
     RC(upload(c, &c->d_big, c->big_groups));
     CK(c, cudaMalloc((void **)&c->d_relw, sizeof(uint32_t) * c->W));
@@ -508,6 +565,12 @@ int setup_local(gr_ctx *c) {
     CK(c, cudaMalloc((void **)&c->d_info_ring, sizeof(gr::DevCycle) * GR_SLOT_RING));
     CK(c, cudaMalloc((void **)&c->d_subcum_ring, sizeof(int32_t) * GR_SLOT_RING * (size_t)(c->G + 1)));
     CK(c, cudaMemset(c->d_info_ring, 0, sizeof(gr::DevCycle) * GR_SLOT_RING));
+    if (const char *dd = getenv("GR_DEBUG_DUMP")) {
+        if (*dd) {
+            c->dbg_path = std::string(dd) + ".rank" + std::to_string(c->rank) + ".json";
+            CK(c, cudaMalloc((void **)&c->d_dbg, sizeof(uint64_t) * 8 * 1024));
+        }
+    }
     CK(c, cudaMalloc((void **)&c->d_counters, sizeof(int32_t) * 4));
     CK(c, cudaMemset(c->d_counters, 0, sizeof(int32_t) * 4));
 
@@ -543,6 +606,7 @@ int setup_local(gr_ctx *c) {
     // 208 KB of dynamic shared memory per CTA: the stage ring, and with push the output tiles
     // (default 4 x 40 KB stages + 2 x 24 KB tiles)
     if (c->push) {
+        c->nstages = 4;
         c->stage_kb = 40;
         if (const char *no = getenv("GR_OUT_TILES")) c->nout = std::max(2, std::min(4, atoi(no)));
         if (const char *ok = getenv("GR_OUT_KB")) c->out_kb = std::max(4, atoi(ok) / 4 * 4);
@@ -650,8 +714,8 @@ void free_all(gr_ctx *c) {
         if (!c->vg && r != c->rank && c->peer_symm[r]) cudaIpcCloseMemHandle(c->peer_symm[r]);
     gr::nvls_free(c->nvls);
     cudaFree(c->symm);
-    void *dptrs[] = {c->d_segs, c->d_chunks, c->d_cbeg, c->d_cend, c->d_groups, c->d_gcb,
-                     c->d_big, c->d_relw, c->d_hbits_dev, c->d_ptr, c->d_rel_ring, c->d_cum_ring, c->d_info_ring, c->d_counters, c->d_gspc, c->d_subcum_ring,
+    void *dptrs[] = {c->d_segs, c->d_chunks, c->d_cbeg, c->d_cend, c->d_groups, c->d_gcb, c->d_gcb_f, c->d_gnc_f,
+                     c->d_big, c->d_relw, c->d_hbits_dev, c->d_ptr, c->d_rel_ring, c->d_cum_ring, c->d_info_ring, c->d_counters, c->d_dbg, c->d_gspc, c->d_subcum_ring,
                      c->d_flags, c->d_trace, c->d_sumsq, c->d_nonfinite};
     for (void *p : dptrs) cudaFree(p);
     cudaFreeHost(c->h_bits);
@@ -816,11 +880,10 @@ static int create_ctx(gr_ctx **out, const gr_world *world, const gr_tensor *tabl
     c->chunk_elems = world->chunk_elems;  // 0: adaptive per group (build_layouts)
     if (const char *ls = getenv("GR_LC_SUB")) c->lc_sub = std::max<int64_t>(256, atoll(ls) / 8 * 8);  // tuning
     if (const char *pu = getenv("GR_PUSH")) c->push = atoi(pu) != 0;  // tuning / comparison
-    // adaptive chunk rule: about N x 148 chunks per group (every rank owns ~one reduce-scatter
-    // chunk per SM of each group; measured 64 MiB at N=4: 220 vs 268 us with one per SM,
-    // profiles/r02/sw5_n4_queue_shape.txt), power of two in [8K, 128K] elements
-    c->chunk_target_div = 148 * (int64_t)std::max(1, world->world_size);
+    // adaptive chunk rules (build_layouts): coarse ~148 chunks per group, fine ~N x 148
+    c->chunk_target_div_fine = 148 * (int64_t)std::max(1, world->world_size);
     if (const char *cd = getenv("GR_CHUNK_DIV")) c->chunk_target_div = std::max<int64_t>(1, atoll(cd));  // tuning
+    if (const char *cf = getenv("GR_CHUNK_DIV_FINE")) c->chunk_target_div_fine = std::max<int64_t>(1, atoll(cf));
     if (const char *cm = getenv("GR_CHUNK_MAX")) c->chunk_max = std::max<int64_t>(8192, atoll(cm));      // tuning
     if (world->chunk_elems == 0)
         if (const char *ce = getenv("GR_CHUNK_ELEMS")) c->chunk_elems = std::max<int64_t>(8, atoll(ce) / 8 * 8);  // tuning
@@ -835,8 +898,15 @@ static int create_ctx(gr_ctx **out, const gr_world *world, const gr_tensor *tabl
     // knobs that fix the cross-rank queue order / algorithm: read before the table hash so every
     // rank must agree on them (a mismatch would desynchronise the fused kernel's queues)
     if (const char *os = getenv("GR_ONESHOT_MAX_BYTES")) c->one_shot_max_bytes = atoll(os);  // tuning
-    if (const char *l1 = getenv("GR_LAG1")) c->lag1 = atoi(l1);
-    if (const char *l2 = getenv("GR_LAG2")) c->lag2 = atoi(l2);
+    if (const char *l1 = getenv("GR_LAG1")) c->lag1 = std::max(0, atoi(l1));
+    if (const char *l2 = getenv("GR_LAG2")) c->lag2 = std::max(0, atoi(l2));
+    // the queue is deadlock-free only with every reduce-scatter queued before the all-gathers
+    // that wait for it (0 <= L1 < L2, tests/test_queue_model.py)
+    if (c->lag1 >= 0 && c->lag2 >= 0 && c->lag2 <= c->lag1) {
+        delete c;
+        return fail(nullptr, GR_EINVAL, "GR_LAG2 (%s) must exceed GR_LAG1 (%s)", getenv("GR_LAG2"), getenv("GR_LAG1"));
+    }
+    if (const char *fb = getenv("GR_FINE_BELOW")) c->fine_below = std::max(0, atoi(fb));
     c->dry = world->device < 0;
     if (c->world.timeout_ms <= 0) c->world.timeout_ms = kDefaultTimeoutMs;
     int rc = build_layouts(c, table, group_of);
@@ -1190,6 +1260,10 @@ static int step_impl(gr_ctx *c, int32_t *released, gr_cycle_info *info, uint32_t
     // cycles that cannot release anything (no locally complete group) do not launch it.
     if (skip_data) {
         c->stats.data_launches_skipped++;
+        if (!p_inline) {  // the slot's pinned mark snapshot is reused GR_SLOT_RING cycles later:
+            CK(c, cudaEventRecord(c->ring_ev[slot], c->s_coord));  // its DMA must have run by then
+            c->ring_pending[slot] = true;
+        }
     } else {
         gr::DataParams d{};
         d.segs = c->d_segs;
@@ -1212,6 +1286,8 @@ static int step_impl(gr_ctx *c, int32_t *released, gr_cycle_info *info, uint32_t
             d.pack_flag[r] = pad;
             d.rs_flag[r] = pad + (size_t)c->C * c->N;
         }
+        d.dbg = c->d_dbg;
+        if (c->d_dbg) CK(c, cudaMemsetAsync(c->d_dbg, 0, sizeof(uint64_t) * 8 * 1024, c->s_data));
         d.work_counter = c->d_counters;
         d.done_counter = c->d_counters + 1;
         d.abort_dev = c->d_counters + 2;
@@ -1235,6 +1311,8 @@ static int step_impl(gr_ctx *c, int32_t *released, gr_cycle_info *info, uint32_t
         d.sub_pack = std::max<int64_t>(256, std::min<int64_t>(spk, cmax));
         d.out_bytes = (int64_t)c->out_kb * 1024;
         d.pub_quantum = c->pub_quantum;
+        d.group_chunk_begin_fine = c->d_gcb_f;
+        d.group_nchunks_fine = c->d_gnc_f;
         d.nout = c->nout;
         d.sub_ag = std::max<int64_t>(256, std::min<int64_t>(stage / es / 256 * 256, cmax));
         d.one_shot_max_bytes = c->one_shot_max_bytes;
@@ -1250,9 +1328,11 @@ static int step_impl(gr_ctx *c, int32_t *released, gr_cycle_info *info, uint32_t
         const int ctas = drain ? c->data_ctas_full[local ? gr::ALGO_LOCAL : gr::ALGO_TWOSHOT]
                                : c->data_ctas[local ? gr::ALGO_LOCAL : gr::ALGO_TWOSHOT];
         d.lc_sub = c->lc_sub;
+        d.fine_below = c->fine_below >= 0 ? c->fine_below : 2 * c->N * ctas;
         // queue lags (3/8 x grid measured 3-4% faster than 2/4 x grid at N=2,4)
-        d.lag1 = c->lag1 > 0 ? c->lag1 : 3 * ctas;
-        d.lag2 = c->lag2 > 0 ? c->lag2 : 8 * ctas;
+        d.lag1 = c->lag1 >= 0 ? c->lag1 : 3 * ctas;
+        d.lag2 = c->lag2 >= 0 ? c->lag2 : 8 * ctas;
+        if (d.lag2 <= d.lag1) d.lag2 = d.lag1 + ctas;  // one override against the other's default
         CK(c, cudaEventRecord(c->ev_bv, c->s_coord));
         CK(c, cudaStreamWaitEvent(c->s_data, c->ev_bv, 0));
         std::pair<cudaEvent_t, cudaEvent_t> evd{};
@@ -1383,7 +1463,8 @@ static int step_impl(gr_ctx *c, int32_t *released, gr_cycle_info *info, uint32_t
         tc.h_done_ns = ns(h_done);
         tc.n_released = n;
         tc.algo = n > 0 ? c->last_algo : 0;
-        tc.nitems = n > 0 ? total_chunks * (c->last_algo == gr::ALGO_LOCAL ? 1 : (c->last_algo == gr::ALGO_ONESHOT ? 2 : 3)) : 0;
+        // N > 1: phase p's items sit at [p*C, p*C + items) (C = every chunk of both chunkings)
+        tc.nitems = n > 0 ? (c->last_algo == gr::ALGO_LOCAL ? total_chunks : 3 * c->C) : 0;
         tc.slot = slot;
         tc.elems = rel_elems;
         c->trace_cycles.push_back(tc);

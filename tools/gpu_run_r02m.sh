@@ -1,0 +1,16 @@
+# r02 call m (4 GPUs): work items of fused chunks (GR_ITEMS_PER_CTA) x lags x stage size, N=4 sweep + fcn220m
+P=gpurun_out/r14
+python -c "import __graft_entry__ as g; g.build()" > ${P}_build.log 2>&1
+bash tools/sweep_cfg5.sh 4 4096 512 "GR_NVLS=0" "GR_ITEMS_PER_CTA=0" "GR_ITEMS_PER_CTA=4" "GR_ITEMS_PER_CTA=8" "GR_ITEMS_PER_CTA=16" \
+  "GR_STAGES=2 GR_STAGE_KB=96" "GR_LAG1=0 GR_LAG2=148 GR_PUB_QUANTUM=8192" "GR_LAG1=0 GR_LAG2=296 GR_PUB_QUANTUM=8192" \
+  "GR_LAG1=148 GR_LAG2=444 GR_PUB_QUANTUM=8192" "GR_LAG1=0 GR_LAG2=148" > ${P}_sweep_n4.txt 2>&1
+cat ${P}_sweep_n4.txt
+TR="python -m torch.distributed.run --nnodes=1 --master-addr 127.0.0.1"
+for ST in "GR_NVLS=0" "GR_ITEMS_PER_CTA=0" "GR_ITEMS_PER_CTA=4" "GR_ITEMS_PER_CTA=8" "GR_ITEMS_PER_CTA=16" "GR_ITEMS_PER_CTA=8 GR_STAGES=2 GR_STAGE_KB=96" "GR_ITEMS_PER_CTA=0 GR_CHUNK_DIV=148"; do
+  echo "== $ST" >> ${P}_bench.txt
+  env $ST timeout 300 $TR --nproc-per-node 4 --master-port 29582 bench.py --gpus 4 --steps 20 --warmup 5 --no-extras 2>/dev/null | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('N=4', d['ms_per_step'], d['busbw_GBps'], d['roofline']['kernel_ms'])" >> ${P}_bench.txt 2>&1
+  env $ST timeout 300 $TR --nproc-per-node 2 --master-port 29583 bench.py --gpus 2 --steps 20 --warmup 5 --no-extras 2>/dev/null | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('N=2', d['ms_per_step'], d['busbw_GBps'], d['roofline']['kernel_ms'])" >> ${P}_bench.txt 2>&1
+done
+cat ${P}_bench.txt
+bash tools/sweep_cfg5.sh 2 4096 512 "GR_NVLS=0" "GR_ITEMS_PER_CTA=0" "GR_ITEMS_PER_CTA=8" > ${P}_sweep_n2.txt 2>&1
+cat ${P}_sweep_n2.txt
