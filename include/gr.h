@@ -162,7 +162,11 @@ int gr_mark_ready_async(gr_ctx *ctx, int32_t rank, int32_t tensor_id, void *dev_
                         void *stream);
 
 /* gr_step — COLLECTIVE: one coordination cycle ("tic").
- * Launches the bitvector kernel (populate: a thread per word from the host
+ * Runs the bitvector kernel (after the first cycle of a rank it is already queued: each
+ * gr_step enqueues the next cycle's kernel behind a stream wait on a pinned "doorbell", and the
+ * next gr_step only writes the cycle's marks and rings it — no launch on the critical path;
+ * gr_wait, gr_step_drain and timing mode retire a queued kernel unused; GR_ARM=0 disables it).
+ * The kernel does: populate (a thread per word from the host
  * marks, or a __ballot_sync over the per-tensor flags of stream-ordered marks;
  * publish; AND over N ranks through peer loads; group release, with
  * __reduce_and_sync for groups spanning many words), enqueues the fused pack ->
@@ -280,6 +284,8 @@ typedef struct {
     double bitvector_device_us; /* summed %globaltimer span of the bitvector kernels (start->hand-off) */
     int64_t data_launches_skipped; /* cycles whose data launch was skipped: no group was complete
                                       on this rank, so none could be released on any rank */
+    int64_t armed_cycles;       /* cycles whose bitvector kernel was enqueued ahead of time behind a
+                                   doorbell (no launch on the cycle's critical path; see gr_step) */
 } gr_stats;
 
 int gr_query(gr_ctx *ctx, int32_t kind, void *out, size_t bytes);

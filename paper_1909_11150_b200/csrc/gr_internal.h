@@ -159,6 +159,20 @@ struct DataParams {
     uint64_t timeout_ns;
 };
 
+// Armed cycles (one rank per process, W <= GR_BV_INLINE_WORDS): the next cycle's bitvector
+// kernel is enqueued ahead of time behind a stream wait on `doorbell` (pinned host memory); a
+// cycle writes this descriptor and rings the doorbell — no kernel launch on the cycle's
+// critical path. The kernel takes the static BvParams from its launch and these per-cycle fields
+// from the descriptor (one PCIe read). skip = 1 retires an armed kernel unused.
+struct CycleDesc {
+    uint32_t doorbell;               // = the armed kernel's sequence number: run
+    uint32_t skip;                   // 1: exit at once (the host needs the stream back)
+    uint32_t epoch, tag, htag;
+    int32_t parity, new_step, check_async, abort_flag, shutdown_flag, slot, pad;
+    uint32_t bits[GR_BV_INLINE_WORDS];
+    uint32_t marked[GR_BV_INLINE_WORDS];
+};
+
 // Virtual ranks (gr_init_virtual): every rank's parameters for one launch on one device.
 // Rank r with bit r of `absent` set never reached the launch (its CTAs exit at once).
 struct BvParamsV {
@@ -174,6 +188,8 @@ struct DataParamsV {
 
 // Kernel launchers (gr_kernels.cu). Return cudaError_t as int.
 int launch_bitvector(const BvParams &p, void *stream);
+// armed cycle: p's out_released / out_cum / out_subcum / out_info are the ring BASES (slot 0)
+int launch_bitvector_armed(const BvParams &p, const CycleDesc *desc, void *stream);
 int launch_bitvector_virtual(const BvParamsV &pv, void *stream);
 int launch_data_virtual(const DataParamsV &pv, int buffer_f16, int stats, void *stream);
 int launch_data(const DataParams &p, int local, int buffer_f16, int ctas, void *stream);

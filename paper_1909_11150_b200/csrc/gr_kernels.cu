@@ -368,6 +368,47 @@ __global__ void __launch_bounds__(NT, 1024 / NT) bitvector_kernel(const __grid_c
     bitvector_body<NT>(p);
 }
 
+// Armed cycle: enqueued before the cycle exists (behind a stream wait on the descriptor's
+// doorbell); the per-cycle fields come from the pinned descriptor, read once.
+template <int NT>
+__global__ void __launch_bounds__(NT, 1024 / NT) bitvector_kernel_armed(const __grid_constant__ BvParams p,
+                                                                        const CycleDesc *desc) {
+    __shared__ BvParams sp;
+    __shared__ int s_skip;
+    // system-scope loads: the host wrote the descriptor before the doorbell the stream waited on
+    auto rd = [](const void *a) { return ld_relaxed_sys32(reinterpret_cast<const uint32_t *>(a)); };
+    const CycleDesc *d = desc;
+    if (threadIdx.x == 0) s_skip = (int)ld_acquire_sys(&d->skip);
+    {   // static part: copy the launch parameters word by word
+        const uint32_t *src = reinterpret_cast<const uint32_t *>(&p);
+        uint32_t *dst = reinterpret_cast<uint32_t *>(&sp);
+        for (int i = threadIdx.x; i < (int)(sizeof(BvParams) / 4); i += blockDim.x) dst[i] = src[i];
+    }
+    __syncthreads();
+    if (s_skip) return;
+    for (int w = threadIdx.x; w < p.W; w += blockDim.x) {
+        sp.inline_bits[w] = rd(&d->bits[w]);
+        sp.inline_marked[w] = rd(&d->marked[w]);
+    }
+    if (threadIdx.x == 0) {
+        const int slot = (int)rd(&d->slot);
+        sp.epoch = rd(&d->epoch);
+        sp.tag = rd(&d->tag);
+        sp.htag = rd(&d->htag);
+        sp.parity = (int32_t)rd(&d->parity);
+        sp.new_step = (int32_t)rd(&d->new_step);
+        sp.check_async = (int32_t)rd(&d->check_async);
+        sp.abort_flag = (int32_t)rd(&d->abort_flag);
+        sp.shutdown_flag = (int32_t)rd(&d->shutdown_flag);
+        sp.out_released = p.out_released + (size_t)slot * p.G;
+        sp.out_cum = p.out_cum + (size_t)slot * (p.G + 1);
+        sp.out_subcum = p.out_subcum + (size_t)slot * (p.G + 1);
+        sp.out_info = p.out_info + slot;
+    }
+    __syncthreads();
+    bitvector_body<NT>(sp);
+}
+
 // Virtual ranks (gr_init_virtual): N ranks of one device in ONE launch, CTA r = rank r, so
 // every rank's CTA is resident while it spins on its peers' LL words. A rank that never
 // reached the launch (host barrier timed out) is `absent`: its CTA exits and its peers time
@@ -407,6 +448,15 @@ int launch_bitvector(const BvParams &p, void *stream) {
     bitvector_attrs();
     if (p.W > GR_BV_INLINE_WORDS) bitvector_kernel<1024><<<1, 1024, smem, (cudaStream_t)stream>>>(p);
     else bitvector_kernel<BV_THREADS><<<1, BV_THREADS, smem, (cudaStream_t)stream>>>(p);
+    return (int)cudaGetLastError();
+}
+
+int launch_bitvector_armed(const BvParams &p, const CycleDesc *desc, void *stream) {
+    const size_t smem = bitvector_smem(p);
+    static std::atomic<uint64_t> done{0};
+    if (first_use_on_device(done))
+        cudaFuncSetAttribute(bitvector_kernel_armed<BV_THREADS>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+    bitvector_kernel_armed<BV_THREADS><<<1, BV_THREADS, smem, (cudaStream_t)stream>>>(p, desc);
     return (int)cudaGetLastError();
 }
 

@@ -50,6 +50,8 @@ uint64_t fnv1a(uint64_t h, const void *data, size_t n) {
 }
 
 typedef CUresult (*PFN_writeValue32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+typedef CUresult (*PFN_waitValue32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+constexpr int kArmSlots = 4;  // cycle descriptors in flight (armed kernel seq uses slot seq % 4)
 
 constexpr int kPtrStages = 4;  // pinned snapshots of the pointer table in flight (DMA sources)
 
@@ -164,6 +166,12 @@ struct gr_ctx {
     gr::HostError *d_err = nullptr;
     size_t hand_bytes = 0;
     PFN_writeValue32 write_value32 = nullptr;
+    PFN_waitValue32 wait_value32 = nullptr;
+    // armed cycles (gr_internal.h CycleDesc): the next cycle's bitvector kernel waits in the
+    // coordination stream for a doorbell in pinned memory, so a cycle launches nothing
+    gr::CycleDesc *h_desc = nullptr, *d_desc = nullptr;  // [kArmSlots], pinned + mapped
+    bool arm_ok = false, armed = false;
+    uint32_t arm_seq = 0;
     int data_ctas[4] = {0, 0, 0, 0};       // world.comm_ctas (or every SM)
     int data_ctas_full[4] = {0, 0, 0, 0};  // every SM (drain cycles)
     int lag1 = -1, lag2 = -1;  // GR_LAG1 / GR_LAG2 overrides (tuning; -1 = default multiple of the grid)
@@ -591,6 +599,9 @@ int setup_local(gr_ctx *c) {
     CK(c, cudaHostAlloc((void **)&c->h_hand, c->hand_bytes, hf));
     memset((void *)c->h_hand, 0, c->hand_bytes);  // tag 0: never a cycle's tag
     CK(c, cudaHostAlloc((void **)&c->h_err, sizeof(gr::HostError), hf));
+    CK(c, cudaHostAlloc((void **)&c->h_desc, sizeof(gr::CycleDesc) * kArmSlots, hf));
+    memset((void *)c->h_desc, 0, sizeof(gr::CycleDesc) * kArmSlots);
+    CK(c, cudaHostGetDevicePointer((void **)&c->d_desc, (void *)c->h_desc, 0));
     memset((void *)c->h_err, 0, sizeof(gr::HostError));
     CK(c, cudaHostGetDevicePointer((void **)&c->d_hbits, c->h_bits, 0));
     CK(c, cudaHostGetDevicePointer((void **)&c->d_hand, (void *)c->h_hand, 0));
@@ -602,6 +613,14 @@ int setup_local(gr_ctx *c) {
     if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &fn, cudaEnableDefault, &q) == cudaSuccess &&
         q == cudaDriverEntryPointSuccess)
         c->write_value32 = (PFN_writeValue32)fn;
+    if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+        c->wait_value32 = (PFN_waitValue32)fn;
+    // armed cycles: real ranks with inline bitvectors (GR_ARM=0 turns them off)
+    {
+        const char *ae = getenv("GR_ARM");
+        c->arm_ok = !c->vg && c->wait_value32 && c->W <= GR_BV_INLINE_WORDS && !(ae && atoi(ae) == 0);
+    }
 
     // 208 KB of dynamic shared memory per CTA: the stage ring, and with push the output tiles
     // (default 4 x 40 KB stages + 2 x 24 KB tiles)
@@ -705,9 +724,65 @@ int setup_device(gr_ctx *c) {
     return GR_OK;
 }
 
+// ---------------------------------------------------------------- armed cycles
+// The per-step static part of a bitvector launch (everything but the per-cycle fields the
+// armed kernel reads from its CycleDesc); out_* are the ring bases.
+void fill_bv_static(gr_ctx *c, gr::BvParams &p) {
+    p.host_bits = c->d_hbits_dev;
+    p.marked_bits = c->d_hbits_dev + c->W;
+    p.dev_flags = c->d_flags;
+    p.groups = c->d_groups;
+    p.stage_groups = c->stage_groups ? 1 : 0;
+    p.big_groups = c->d_big;
+    p.n_big = (int32_t)c->big_groups.size();
+    p.rel_words = c->d_relw;
+    for (int r = 0; r < c->N; ++r) p.slot[r] = reinterpret_cast<uint64_t *>(c->peer_symm[r] + c->off_slot);
+    p.out_released = c->d_rel_ring;
+    p.out_cum = c->d_cum_ring;
+    p.out_info = c->d_info_ring;
+    p.out_subcum = c->d_subcum_ring;
+    p.hand = c->d_hand;
+    p.T = c->T;
+    p.G = c->G;
+    p.W = c->W;
+    p.nbits = c->nbits;
+    p.rank = c->rank;
+    p.N = c->N;
+    p.timeout_ns = (uint64_t)c->world.timeout_ms * 1000000ull;
+    p.use_inline = 1;
+    p.drain = 0;
+    p.err = c->h_err;
+}
+
+// enqueue the next cycle's bitvector kernel behind a wait on its descriptor's doorbell
+int arm(gr_ctx *c) {
+    if (!c->arm_ok || c->armed || c->sticky || c->timing) return GR_OK;
+    if (++c->arm_seq == 0) ++c->arm_seq;
+    gr::CycleDesc *d = c->d_desc + c->arm_seq % kArmSlots;
+    gr::BvParams p{};
+    fill_bv_static(c, p);
+    CUresult r = c->wait_value32((CUstream)c->s_coord, (CUdeviceptr)&d->doorbell, c->arm_seq, CU_STREAM_WAIT_VALUE_EQ);
+    if (r != CUDA_SUCCESS) return fail(c, GR_ECUDA, "cuStreamWaitValue32 failed (%d)", (int)r);
+    int lrc = gr::launch_bitvector_armed(p, d, c->s_coord);
+    if (lrc) return fail(c, GR_ECUDA, "armed bitvector launch: %s", cudaGetErrorString((cudaError_t)lrc));
+    c->armed = true;
+    return GR_OK;
+}
+
+// retire an armed kernel unused (it runs and exits at once); needed before anything waits on
+// the coordination stream or enqueues other work in front of the next cycle
+void disarm(gr_ctx *c) {
+    if (!c->armed) return;
+    gr::CycleDesc *h = c->h_desc + c->arm_seq % kArmSlots;
+    h->skip = 1;
+    __atomic_store_n(&h->doorbell, c->arm_seq, __ATOMIC_RELEASE);
+    c->armed = false;
+}
+
 void free_all(gr_ctx *c) {
     if (c->dry || c->dev < 0) return;
     cudaSetDevice(c->dev);
+    disarm(c);
     if (c->s_coord) cudaStreamSynchronize(c->s_coord);
     if (c->s_data) cudaStreamSynchronize(c->s_data);
     for (int r = 0; r < c->N; ++r)
@@ -1142,6 +1217,10 @@ static int step_impl(gr_ctx *c, int32_t *released, gr_cycle_info *info, uint32_t
     int32_t abort_flag, shutdown_flag;
     bool p_inline = c->W <= GR_BV_INLINE_WORDS, step_fresh = false, async_used = false;
     gr::BvParams p{};
+    // armed cycle: the kernel is already queued; drains, timing and fallbacks retire it first
+    const bool use_armed = c->armed && !drain && !c->timing && p_inline;
+    if (!use_armed) disarm(c);
+    gr::CycleDesc *hd = use_armed ? c->h_desc + c->arm_seq % kArmSlots : nullptr;
     // the pointer-table snapshot buffer this cycle may use (its previous upload has long run)
     const int pk = c->ptr_stage_next;
     if (c->ptr_stage_pending[pk]) {
@@ -1167,7 +1246,10 @@ static int step_impl(gr_ctx *c, int32_t *released, gr_cycle_info *info, uint32_t
         step_fresh = c->step_fresh;
         c->step_fresh = false;
         async_used = c->async_used;
-        if (p_inline) {  // the mark bits travel in the launch parameters
+        if (hd) {        // ... in the armed kernel's pinned descriptor
+            memcpy(hd->bits, c->h_bits, sizeof(uint32_t) * c->W);
+            memcpy(hd->marked, c->h_marked, sizeof(uint32_t) * c->W);
+        } else if (p_inline) {  // the mark bits travel in the launch parameters
             memcpy(p.inline_bits, c->h_bits, sizeof(uint32_t) * c->W);
             memcpy(p.inline_marked, c->h_marked, sizeof(uint32_t) * c->W);
         } else {         // ... or in this ring slot's pinned snapshot, DMA'd before the kernel
@@ -1241,7 +1323,21 @@ static int step_impl(gr_ctx *c, int32_t *released, gr_cycle_info *info, uint32_t
     if (!p_inline)  // larger bitvectors: one DMA of the cycle's snapshot, stream-ordered before the kernel
         CK(c, cudaMemcpyAsync(c->d_hbits_dev, bits_stage, sizeof(uint32_t) * 2 * c->W, cudaMemcpyHostToDevice,
                               c->s_coord));
-    if (c->vg) {
+    if (hd) {  // ring the armed kernel: the descriptor first, the doorbell last (x86 keeps store order)
+        hd->skip = 0;
+        hd->epoch = p.epoch;
+        hd->tag = p.tag;
+        hd->htag = p.htag;
+        hd->parity = p.parity;
+        hd->new_step = p.new_step;
+        hd->check_async = p.check_async;
+        hd->abort_flag = p.abort_flag;
+        hd->shutdown_flag = p.shutdown_flag;
+        hd->slot = slot;
+        __atomic_store_n(&hd->doorbell, c->arm_seq, __ATOMIC_RELEASE);
+        c->armed = false;
+        c->stats.armed_cycles++;
+    } else if (c->vg) {
         RC(vg_launch(c, 0, c->s_coord, &p, nullptr));
     } else {
         int lrc = gr::launch_bitvector(p, c->s_coord);
@@ -1370,6 +1466,9 @@ static int step_impl(gr_ctx *c, int32_t *released, gr_cycle_info *info, uint32_t
         c->ring_pending[slot] = true;
         c->stats.data_launches++;
     }
+
+    // queue the next cycle's kernel now, while this one's runs (its launch cost overlaps the wait)
+    if (!drain) RC(arm(c));
 
     if (drain) {  // device-driven final cycle: the host does not wait for the hand-off
         c->cycle++;
@@ -1533,6 +1632,7 @@ int gr_wait(gr_ctx *c) {
     if (c->dry) return fail(c, GR_ESTATE, "dry context (device < 0) cannot wait");
     if (c->sticky == GR_ECUDA) return fail(c, GR_ESTATE, "context is in a sticky error state: %s", c->err.c_str());
     CK(c, cudaSetDevice(c->dev));
+    disarm(c);  // a queued armed kernel would hold the coordination stream forever
     CK(c, cudaStreamSynchronize(c->s_coord));
     CK(c, cudaStreamSynchronize(c->s_data));
     if (c->h_err->code) return device_error(c);

@@ -441,6 +441,40 @@ def test_new_gradient_buffers_every_step_async_wait(gpu):
     ctx.gr_finalize()
 
 
+@pytest.mark.parametrize("arm", ["1", "0"])
+def test_armed_cycles_n1(gpu, arm, monkeypatch):
+    """Armed cycles (gr.h gr_step): after a rank's first cycle every non-drain cycle's bitvector
+    kernel is already queued behind a pinned doorbell; gr_wait / gr_step_drain / timing retire
+    it unused. Many-cycle cfg1 schedules (host marks, drains with host or stream-ordered marks,
+    a blocking gr_wait per step, timing mode toggled) stay bit-exact against the oracle with arming on
+    (GR_ARM=1) and off (GR_ARM=0), and the armed path is really taken."""
+    import torch
+    from paper_1909_11150_b200 import GR_F16, Context
+    from tests.parity_lib import run_case_on_rank, run_drain_case_on_rank
+    monkeypatch.setenv("GR_ARM", arm)
+    base = cfg1_case(11)
+    ctx = Context(rank=0, world_size=1, device=0, numel=base.numel, group_of=base.group_of, buffer_dtype=GR_F16,
+                  timeout_ms=10000)
+    s = torch.cuda.Stream(device=gpu)
+    try:
+        for seed in range(8):
+            c = cfg1_case(100 + seed)
+            case = Case(1, base.numel, base.group_of, c.mark_cycle[:1].copy(), 100 + seed)
+            ctx.set_timing(seed == 3)
+            if seed % 4 == 2:
+                run_drain_case_on_rank(ctx, case, 0, 100 + seed, gpu, True, 1,
+                                       async_stream=s.cuda_stream if seed % 2 else None)
+            else:
+                run_case_on_rank(ctx, case, 0, 100 + seed, gpu, True)
+        st = ctx.stats()
+        if arm == "1":
+            assert st.armed_cycles > 0 and st.armed_cycles < st.cycles
+        else:
+            assert st.armed_cycles == 0
+    finally:
+        ctx.gr_finalize()
+
+
 @pytest.mark.parametrize("T", [64, 4096])
 def test_marks_racing_steps(gpu, T):
     """gr_mark_ready / gr_mark_ready_async from another thread race gr_step (gr.h: thread-safe):
