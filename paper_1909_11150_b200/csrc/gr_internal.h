@@ -159,11 +159,11 @@ struct DataParams {
     uint64_t timeout_ns;
 };
 
-// Armed cycles (one rank per process, W <= GR_BV_INLINE_WORDS): the next cycle's bitvector
-// kernel is enqueued ahead of time behind a stream wait on `doorbell` (pinned host memory); a
-// cycle writes this descriptor and rings the doorbell — no kernel launch on the cycle's
-// critical path. The kernel takes the static BvParams from its launch and these per-cycle fields
-// from the descriptor (one PCIe read). skip = 1 retires an armed kernel unused.
+// Armed cycles (one rank per process, W <= GR_BV_INLINE_WORDS, tight cycle loops): right after
+// a cycle the next cycle's bitvector kernel is launched and polls `doorbell` (pinned host
+// memory) for a bounded time; a cycle writes this descriptor and rings the doorbell — no kernel
+// launch on the cycle's critical path. The kernel takes the static BvParams from its launch and
+// these per-cycle fields from the descriptor (one PCIe read). skip = 1 retires it unused.
 struct CycleDesc {
     uint32_t doorbell;               // = the armed kernel's sequence number: run
     uint32_t skip;                   // 1: exit at once (the host needs the stream back)
@@ -188,8 +188,10 @@ struct DataParamsV {
 
 // Kernel launchers (gr_kernels.cu). Return cudaError_t as int.
 int launch_bitvector(const BvParams &p, void *stream);
-// armed cycle: p's out_released / out_cum / out_subcum / out_info are the ring BASES (slot 0)
-int launch_bitvector_armed(const BvParams &p, const CycleDesc *desc, void *stream);
+// armed cycle: p's out_released / out_cum / out_subcum / out_info are the ring BASES (slot 0);
+// the kernel polls desc->doorbell == seq for at most expire_ns and acknowledges in *ack
+int launch_bitvector_armed(const BvParams &p, const CycleDesc *desc, uint32_t seq, uint64_t expire_ns,
+                           uint32_t *ack, void *stream);
 int launch_bitvector_virtual(const BvParamsV &pv, void *stream);
 int launch_data_virtual(const DataParamsV &pv, int buffer_f16, int stats, void *stream);
 int launch_data(const DataParams &p, int local, int buffer_f16, int ctas, void *stream);

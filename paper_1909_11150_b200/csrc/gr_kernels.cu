@@ -368,24 +368,44 @@ __global__ void __launch_bounds__(NT, 1024 / NT) bitvector_kernel(const __grid_c
     bitvector_body<NT>(p);
 }
 
-// Armed cycle: enqueued before the cycle exists (behind a stream wait on the descriptor's
-// doorbell); the per-cycle fields come from the pinned descriptor, read once.
+// Armed cycle: launched right after a cycle, before the next one exists. Thread 0 polls the
+// pinned descriptor's doorbell for at most `expire_ns` (bounded residency: one small CTA, and
+// a device-wide synchronize waits at most that long); it acknowledges in pinned memory —
+// ack = seq << 1 | 1 "accepted, running this cycle" or seq << 1 "expired / retired unused" —
+// and the per-cycle fields then come from the descriptor (one PCIe read).
 template <int NT>
 __global__ void __launch_bounds__(NT, 1024 / NT) bitvector_kernel_armed(const __grid_constant__ BvParams p,
-                                                                        const CycleDesc *desc) {
+                                                                        const CycleDesc *desc, uint32_t seq,
+                                                                        uint64_t expire_ns, uint32_t *ack) {
     __shared__ BvParams sp;
-    __shared__ int s_skip;
-    // system-scope loads: the host wrote the descriptor before the doorbell the stream waited on
+    __shared__ int s_go;
     auto rd = [](const void *a) { return ld_relaxed_sys32(reinterpret_cast<const uint32_t *>(a)); };
     const CycleDesc *d = desc;
-    if (threadIdx.x == 0) s_skip = (int)ld_acquire_sys(&d->skip);
+    if (threadIdx.x == 0) {
+        const uint64_t dl = globaltimer() + expire_ns;
+        int go = 0;
+        for (;;) {
+            if (ld_acquire_sys(&d->doorbell) == seq) {  // rung (skip = retired by the host)
+                go = rd(&d->skip) ? 0 : 1;
+                if (go) st_relaxed_sys32(ack, (seq << 1) | 1u);
+                break;
+            }
+            if (globaltimer() > dl) {  // nobody came: tell the host to launch this cycle itself
+                fence_acq_rel_sys();
+                st_relaxed_sys32(ack, seq << 1);
+                break;
+            }
+            __nanosleep(128);
+        }
+        s_go = go;
+    }
     {   // static part: copy the launch parameters word by word
         const uint32_t *src = reinterpret_cast<const uint32_t *>(&p);
         uint32_t *dst = reinterpret_cast<uint32_t *>(&sp);
         for (int i = threadIdx.x; i < (int)(sizeof(BvParams) / 4); i += blockDim.x) dst[i] = src[i];
     }
     __syncthreads();
-    if (s_skip) return;
+    if (!s_go) return;
     for (int w = threadIdx.x; w < p.W; w += blockDim.x) {
         sp.inline_bits[w] = rd(&d->bits[w]);
         sp.inline_marked[w] = rd(&d->marked[w]);
@@ -409,10 +429,6 @@ __global__ void __launch_bounds__(NT, 1024 / NT) bitvector_kernel_armed(const __
     bitvector_body<NT>(sp);
 }
 
-// Virtual ranks (gr_init_virtual): N ranks of one device in ONE launch, CTA r = rank r, so
-// every rank's CTA is resident while it spins on its peers' LL words. A rank that never
-// reached the launch (host barrier timed out) is `absent`: its CTA exits and its peers time
-// out on its words, as they would on a stalled process.
 template <int NT>
 __global__ void __launch_bounds__(NT, 1024 / NT) bitvector_kernel_v(const __grid_constant__ BvParamsV pv) {
     if (blockIdx.x >= (unsigned)pv.N || ((pv.absent >> blockIdx.x) & 1u)) return;
@@ -451,12 +467,13 @@ int launch_bitvector(const BvParams &p, void *stream) {
     return (int)cudaGetLastError();
 }
 
-int launch_bitvector_armed(const BvParams &p, const CycleDesc *desc, void *stream) {
+int launch_bitvector_armed(const BvParams &p, const CycleDesc *desc, uint32_t seq, uint64_t expire_ns,
+                           uint32_t *ack, void *stream) {
     const size_t smem = bitvector_smem(p);
     static std::atomic<uint64_t> done{0};
     if (first_use_on_device(done))
         cudaFuncSetAttribute(bitvector_kernel_armed<BV_THREADS>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
-    bitvector_kernel_armed<BV_THREADS><<<1, BV_THREADS, smem, (cudaStream_t)stream>>>(p, desc);
+    bitvector_kernel_armed<BV_THREADS><<<1, BV_THREADS, smem, (cudaStream_t)stream>>>(p, desc, seq, expire_ns, ack);
     return (int)cudaGetLastError();
 }
 

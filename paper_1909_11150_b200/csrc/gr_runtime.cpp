@@ -50,7 +50,6 @@ uint64_t fnv1a(uint64_t h, const void *data, size_t n) {
 }
 
 typedef CUresult (*PFN_writeValue32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
-typedef CUresult (*PFN_waitValue32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
 constexpr int kArmSlots = 4;  // cycle descriptors in flight (armed kernel seq uses slot seq % 4)
 
 constexpr int kPtrStages = 4;  // pinned snapshots of the pointer table in flight (DMA sources)
@@ -166,12 +165,15 @@ struct gr_ctx {
     gr::HostError *d_err = nullptr;
     size_t hand_bytes = 0;
     PFN_writeValue32 write_value32 = nullptr;
-    PFN_waitValue32 wait_value32 = nullptr;
-    // armed cycles (gr_internal.h CycleDesc): the next cycle's bitvector kernel waits in the
-    // coordination stream for a doorbell in pinned memory, so a cycle launches nothing
+    // armed cycles (gr_internal.h CycleDesc): in a tight cycle loop the next cycle's bitvector
+    // kernel is already running, polling a doorbell in pinned memory, so a cycle launches nothing
     gr::CycleDesc *h_desc = nullptr, *d_desc = nullptr;  // [kArmSlots], pinned + mapped
+    uint32_t *h_ack = nullptr, *d_ack = nullptr;         // the armed kernel's acknowledgement
     bool arm_ok = false, armed = false;
     uint32_t arm_seq = 0;
+    int64_t arm_expire_us = 100, arm_gap_us = 50;  // kernel lifetime; arm only after gaps below this
+    double last_gap_us = 1e30;                      // host time between the last two gr_step calls
+    std::chrono::steady_clock::time_point last_step_exit{};
     int data_ctas[4] = {0, 0, 0, 0};       // world.comm_ctas (or every SM)
     int data_ctas_full[4] = {0, 0, 0, 0};  // every SM (drain cycles)
     int lag1 = -1, lag2 = -1;  // GR_LAG1 / GR_LAG2 overrides (tuning; -1 = default multiple of the grid)
@@ -602,6 +604,9 @@ int setup_local(gr_ctx *c) {
     CK(c, cudaHostAlloc((void **)&c->h_desc, sizeof(gr::CycleDesc) * kArmSlots, hf));
     memset((void *)c->h_desc, 0, sizeof(gr::CycleDesc) * kArmSlots);
     CK(c, cudaHostGetDevicePointer((void **)&c->d_desc, (void *)c->h_desc, 0));
+    CK(c, cudaHostAlloc((void **)&c->h_ack, 64, hf));
+    memset((void *)c->h_ack, 0, 64);
+    CK(c, cudaHostGetDevicePointer((void **)&c->d_ack, (void *)c->h_ack, 0));
     memset((void *)c->h_err, 0, sizeof(gr::HostError));
     CK(c, cudaHostGetDevicePointer((void **)&c->d_hbits, c->h_bits, 0));
     CK(c, cudaHostGetDevicePointer((void **)&c->d_hand, (void *)c->h_hand, 0));
@@ -613,13 +618,13 @@ int setup_local(gr_ctx *c) {
     if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &fn, cudaEnableDefault, &q) == cudaSuccess &&
         q == cudaDriverEntryPointSuccess)
         c->write_value32 = (PFN_writeValue32)fn;
-    if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &fn, cudaEnableDefault, &q) == cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-        c->wait_value32 = (PFN_waitValue32)fn;
-    // armed cycles: real ranks with inline bitvectors (GR_ARM=0 turns them off)
+    // armed cycles: real ranks with inline bitvectors (GR_ARM=0 turns them off; GR_ARM_US /
+    // GR_ARM_GAP_US: the armed kernel's lifetime and the cycle gap below which it is used)
     {
         const char *ae = getenv("GR_ARM");
-        c->arm_ok = !c->vg && c->wait_value32 && c->W <= GR_BV_INLINE_WORDS && !(ae && atoi(ae) == 0);
+        c->arm_ok = !c->vg && c->W <= GR_BV_INLINE_WORDS && !(ae && atoi(ae) == 0);
+        if (const char *x = getenv("GR_ARM_US")) c->arm_expire_us = std::max<int64_t>(1, atoll(x));
+        if (const char *x = getenv("GR_ARM_GAP_US")) c->arm_gap_us = std::max<int64_t>(0, atoll(x));
     }
 
     // 208 KB of dynamic shared memory per CTA: the stage ring, and with push the output tiles
@@ -754,16 +759,16 @@ void fill_bv_static(gr_ctx *c, gr::BvParams &p) {
     p.err = c->h_err;
 }
 
-// enqueue the next cycle's bitvector kernel behind a wait on its descriptor's doorbell
+// launch the next cycle's bitvector kernel now: it polls its descriptor's doorbell for at most
+// arm_expire_us. Only in tight cycle loops (the last gap between gr_step calls below
+// arm_gap_us): a training loop that ticks every few hundred us never holds an SM for it.
 int arm(gr_ctx *c) {
-    if (!c->arm_ok || c->armed || c->sticky || c->timing) return GR_OK;
-    if (++c->arm_seq == 0) ++c->arm_seq;
+    if (!c->arm_ok || c->armed || c->sticky || c->timing || c->last_gap_us > (double)c->arm_gap_us) return GR_OK;
+    if (++c->arm_seq >= 0x7fffffffu) c->arm_seq = 1;  // the acknowledgement carries seq << 1
     gr::CycleDesc *d = c->d_desc + c->arm_seq % kArmSlots;
     gr::BvParams p{};
     fill_bv_static(c, p);
-    CUresult r = c->wait_value32((CUstream)c->s_coord, (CUdeviceptr)&d->doorbell, c->arm_seq, CU_STREAM_WAIT_VALUE_EQ);
-    if (r != CUDA_SUCCESS) return fail(c, GR_ECUDA, "cuStreamWaitValue32 failed (%d)", (int)r);
-    int lrc = gr::launch_bitvector_armed(p, d, c->s_coord);
+    int lrc = gr::launch_bitvector_armed(p, d, c->arm_seq, (uint64_t)c->arm_expire_us * 1000ull, c->d_ack, c->s_coord);
     if (lrc) return fail(c, GR_ECUDA, "armed bitvector launch: %s", cudaGetErrorString((cudaError_t)lrc));
     c->armed = true;
     return GR_OK;
@@ -804,6 +809,8 @@ void free_all(gr_ctx *c) {
         if (c->ev_vin[i]) cudaEventDestroy(c->ev_vin[i]);
     cudaFreeHost((void *)c->h_hand);
     cudaFreeHost((void *)c->h_err);
+    cudaFreeHost((void *)c->h_desc);
+    cudaFreeHost((void *)c->h_ack);
     for (int i = 0; i < GR_SLOT_RING; ++i)
         if (c->ring_ev[i]) cudaEventDestroy(c->ring_ev[i]);
     if (c->ev_compute) cudaEventDestroy(c->ev_compute);
@@ -1206,6 +1213,8 @@ static int step_impl(gr_ctx *c, int32_t *released, gr_cycle_info *info, uint32_t
     if (c->dry) return fail(c, GR_ESTATE, "dry context (device < 0) cannot step");
     if (c->sticky) return fail(c, GR_ESTATE, "context is in a sticky error state (%d): %s", c->sticky, c->err.c_str());
     const auto h_enter = std::chrono::steady_clock::now();
+    if (c->last_step_exit.time_since_epoch().count())
+        c->last_gap_us = std::chrono::duration<double, std::micro>(h_enter - c->last_step_exit).count();
     if (c->h_err->code) return device_error(c);
     CK(c, cudaSetDevice(c->dev));
     const int slot = (int)(c->cycle % GR_SLOT_RING);
@@ -1323,6 +1332,7 @@ static int step_impl(gr_ctx *c, int32_t *released, gr_cycle_info *info, uint32_t
     if (!p_inline)  // larger bitvectors: one DMA of the cycle's snapshot, stream-ordered before the kernel
         CK(c, cudaMemcpyAsync(c->d_hbits_dev, bits_stage, sizeof(uint32_t) * 2 * c->W, cudaMemcpyHostToDevice,
                               c->s_coord));
+    bool ran_armed = false;
     if (hd) {  // ring the armed kernel: the descriptor first, the doorbell last (x86 keeps store order)
         hd->skip = 0;
         hd->epoch = p.epoch;
@@ -1336,7 +1346,23 @@ static int step_impl(gr_ctx *c, int32_t *released, gr_cycle_info *info, uint32_t
         hd->slot = slot;
         __atomic_store_n(&hd->doorbell, c->arm_seq, __ATOMIC_RELEASE);
         c->armed = false;
-        c->stats.armed_cycles++;
+        // the kernel acknowledges: accepted (it runs this cycle) or expired before the doorbell
+        const uint32_t want = c->arm_seq << 1;
+        const auto t0 = std::chrono::steady_clock::now();
+        uint32_t a;
+        while (((a = __atomic_load_n(c->h_ack, __ATOMIC_ACQUIRE)) & ~1u) != want) {
+            if (std::chrono::steady_clock::now() - t0 > std::chrono::milliseconds(c->world.timeout_ms + 5000))
+                return fail(c, GR_ETIMEOUT, "armed bitvector kernel never acknowledged");
+        }
+        if (a & 1u) {
+            ran_armed = true;
+            c->stats.armed_cycles++;
+        } else {  // expired: this cycle's marks travel in the launch parameters after all
+            memcpy(p.inline_bits, hd->bits, sizeof(uint32_t) * c->W);
+            memcpy(p.inline_marked, hd->marked, sizeof(uint32_t) * c->W);
+        }
+    }
+    if (ran_armed) {
     } else if (c->vg) {
         RC(vg_launch(c, 0, c->s_coord, &p, nullptr));
     } else {
@@ -1471,6 +1497,7 @@ static int step_impl(gr_ctx *c, int32_t *released, gr_cycle_info *info, uint32_t
     if (!drain) RC(arm(c));
 
     if (drain) {  // device-driven final cycle: the host does not wait for the hand-off
+        c->last_step_exit = std::chrono::steady_clock::now();
         c->cycle++;
         c->stats.cycles++;
         std::lock_guard<std::mutex> lk(c->mu);
@@ -1572,6 +1599,7 @@ static int step_impl(gr_ctx *c, int32_t *released, gr_cycle_info *info, uint32_t
         std::lock_guard<std::mutex> lk(c->mu);
         if (complete) c->step_complete = true;
     }
+    c->last_step_exit = std::chrono::steady_clock::now();
     if (info) {
         info->n_released = n;
         info->step_complete = complete;
