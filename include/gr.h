@@ -162,10 +162,12 @@ int gr_mark_ready_async(gr_ctx *ctx, int32_t rank, int32_t tensor_id, void *dev_
                         void *stream);
 
 /* gr_step — COLLECTIVE: one coordination cycle ("tic").
- * Runs the bitvector kernel (after the first cycle of a rank it is already queued: each
- * gr_step enqueues the next cycle's kernel behind a stream wait on a pinned "doorbell", and the
- * next gr_step only writes the cycle's marks and rings it — no launch on the critical path;
- * gr_wait, gr_step_drain and timing mode retire a queued kernel unused; GR_ARM=0 disables it).
+ * Runs the bitvector kernel. In a tight cycle loop (less than GR_ARM_GAP_US = 50 us between
+ * gr_step calls) it is already running: each gr_step launches the next cycle's kernel, which
+ * polls a pinned "doorbell" for at most GR_ARM_US = 100 us; the next gr_step writes the cycle's
+ * marks and rings it — no launch on the critical path (an expired kernel acknowledges and the
+ * cycle is launched as usual; gr_wait, gr_step_drain and timing mode retire it; GR_ARM=0 turns
+ * this off; a device-wide synchronize waits at most GR_ARM_US for it).
  * The kernel does: populate (a thread per word from the host
  * marks, or a __ballot_sync over the per-tensor flags of stream-ordered marks;
  * publish; AND over N ranks through peer loads; group release, with
@@ -284,8 +286,8 @@ typedef struct {
     double bitvector_device_us; /* summed %globaltimer span of the bitvector kernels (start->hand-off) */
     int64_t data_launches_skipped; /* cycles whose data launch was skipped: no group was complete
                                       on this rank, so none could be released on any rank */
-    int64_t armed_cycles;       /* cycles whose bitvector kernel was enqueued ahead of time behind a
-                                   doorbell (no launch on the cycle's critical path; see gr_step) */
+    int64_t armed_cycles;       /* cycles run by an armed bitvector kernel (launched ahead of the
+                                   cycle, rung through a pinned doorbell; see gr_step) */
 } gr_stats;
 
 int gr_query(gr_ctx *ctx, int32_t kind, void *out, size_t bytes);

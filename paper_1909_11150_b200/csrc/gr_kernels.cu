@@ -26,6 +26,7 @@
 // peer data. LL bitvector words carry their cycle tag in the upper 32 bits, so a
 // single 64-bit load both validates and returns the word.
 #include <atomic>
+#include <cstddef>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
@@ -406,20 +407,30 @@ __global__ void __launch_bounds__(NT, 1024 / NT) bitvector_kernel_armed(const __
     }
     __syncthreads();
     if (!s_go) return;
+    // the descriptor in ONE PCIe round trip: every thread reads one word of it
+    __shared__ CycleDesc sd;
+    {
+        constexpr int HW = (int)(offsetof(CycleDesc, bits) / 4);  // header words, then bits[], marked[]
+        const uint32_t *src = reinterpret_cast<const uint32_t *>(d);
+        uint32_t *dst = reinterpret_cast<uint32_t *>(&sd);
+        for (int i = threadIdx.x; i < HW + 2 * GR_BV_INLINE_WORDS; i += blockDim.x)
+            if (i < HW || (i - HW) % GR_BV_INLINE_WORDS < p.W) dst[i] = rd(src + i);
+    }
+    __syncthreads();
     for (int w = threadIdx.x; w < p.W; w += blockDim.x) {
-        sp.inline_bits[w] = rd(&d->bits[w]);
-        sp.inline_marked[w] = rd(&d->marked[w]);
+        sp.inline_bits[w] = sd.bits[w];
+        sp.inline_marked[w] = sd.marked[w];
     }
     if (threadIdx.x == 0) {
-        const int slot = (int)rd(&d->slot);
-        sp.epoch = rd(&d->epoch);
-        sp.tag = rd(&d->tag);
-        sp.htag = rd(&d->htag);
-        sp.parity = (int32_t)rd(&d->parity);
-        sp.new_step = (int32_t)rd(&d->new_step);
-        sp.check_async = (int32_t)rd(&d->check_async);
-        sp.abort_flag = (int32_t)rd(&d->abort_flag);
-        sp.shutdown_flag = (int32_t)rd(&d->shutdown_flag);
+        const int slot = sd.slot;
+        sp.epoch = sd.epoch;
+        sp.tag = sd.tag;
+        sp.htag = sd.htag;
+        sp.parity = sd.parity;
+        sp.new_step = sd.new_step;
+        sp.check_async = sd.check_async;
+        sp.abort_flag = sd.abort_flag;
+        sp.shutdown_flag = sd.shutdown_flag;
         sp.out_released = p.out_released + (size_t)slot * p.G;
         sp.out_cum = p.out_cum + (size_t)slot * (p.G + 1);
         sp.out_subcum = p.out_subcum + (size_t)slot * (p.G + 1);

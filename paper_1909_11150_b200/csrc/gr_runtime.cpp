@@ -173,7 +173,7 @@ struct gr_ctx {
     uint32_t arm_seq = 0;
     int64_t arm_expire_us = 100, arm_gap_us = 50;  // kernel lifetime; arm only after gaps below this
     double last_gap_us = 1e30;                      // host time between the last two gr_step calls
-    std::chrono::steady_clock::time_point last_step_exit{};
+    std::chrono::steady_clock::time_point last_step_exit{}, arm_time{};
     int data_ctas[4] = {0, 0, 0, 0};       // world.comm_ctas (or every SM)
     int data_ctas_full[4] = {0, 0, 0, 0};  // every SM (drain cycles)
     int lag1 = -1, lag2 = -1;  // GR_LAG1 / GR_LAG2 overrides (tuning; -1 = default multiple of the grid)
@@ -768,6 +768,7 @@ int arm(gr_ctx *c) {
     gr::CycleDesc *d = c->d_desc + c->arm_seq % kArmSlots;
     gr::BvParams p{};
     fill_bv_static(c, p);
+    c->arm_time = std::chrono::steady_clock::now();  // its lifetime starts no earlier than this
     int lrc = gr::launch_bitvector_armed(p, d, c->arm_seq, (uint64_t)c->arm_expire_us * 1000ull, c->d_ack, c->s_coord);
     if (lrc) return fail(c, GR_ECUDA, "armed bitvector launch: %s", cudaGetErrorString((cudaError_t)lrc));
     c->armed = true;
@@ -1346,13 +1347,18 @@ static int step_impl(gr_ctx *c, int32_t *released, gr_cycle_info *info, uint32_t
         hd->slot = slot;
         __atomic_store_n(&hd->doorbell, c->arm_seq, __ATOMIC_RELEASE);
         c->armed = false;
-        // the kernel acknowledges: accepted (it runs this cycle) or expired before the doorbell
-        const uint32_t want = c->arm_seq << 1;
+        // rung well inside the kernel's lifetime (which starts after its launch): it cannot have
+        // expired, go on. Otherwise its acknowledgement tells: accepted, or expired before the
+        // doorbell (then this cycle is launched as usual).
         const auto t0 = std::chrono::steady_clock::now();
-        uint32_t a;
-        while (((a = __atomic_load_n(c->h_ack, __ATOMIC_ACQUIRE)) & ~1u) != want) {
-            if (std::chrono::steady_clock::now() - t0 > std::chrono::milliseconds(c->world.timeout_ms + 5000))
-                return fail(c, GR_ETIMEOUT, "armed bitvector kernel never acknowledged");
+        const double since = std::chrono::duration<double, std::micro>(t0 - c->arm_time).count();
+        uint32_t a = 1u;
+        if (since > (double)c->arm_expire_us * 0.8 - 10.0) {
+            const uint32_t want = c->arm_seq << 1;
+            while (((a = __atomic_load_n(c->h_ack, __ATOMIC_ACQUIRE)) & ~1u) != want) {
+                if (std::chrono::steady_clock::now() - t0 > std::chrono::milliseconds(c->world.timeout_ms + 5000))
+                    return fail(c, GR_ETIMEOUT, "armed bitvector kernel never acknowledged");
+            }
         }
         if (a & 1u) {
             ran_armed = true;

@@ -441,17 +441,21 @@ def test_new_gradient_buffers_every_step_async_wait(gpu):
     ctx.gr_finalize()
 
 
-@pytest.mark.parametrize("arm", ["1", "0"])
+@pytest.mark.parametrize("arm", ["on", "expire", "off"])
 def test_armed_cycles_n1(gpu, arm, monkeypatch):
-    """Armed cycles (gr.h gr_step): after a rank's first cycle every non-drain cycle's bitvector
-    kernel is already queued behind a pinned doorbell; gr_wait / gr_step_drain / timing retire
-    it unused. Many-cycle cfg1 schedules (host marks, drains with host or stream-ordered marks,
-    a blocking gr_wait per step, timing mode toggled) stay bit-exact against the oracle with arming on
-    (GR_ARM=1) and off (GR_ARM=0), and the armed path is really taken."""
+    """Armed cycles (gr.h gr_step): in a tight cycle loop the next cycle's bitvector kernel is
+    launched ahead of the cycle and polls a pinned doorbell; gr_wait / gr_step_drain / timing
+    retire it, and an armed kernel that expires before its doorbell hands the cycle back to a
+    normal launch. Many-cycle cfg1 schedules (host marks, drains with host or stream-ordered
+    marks, a blocking gr_wait per step, timing mode toggled) stay bit-exact against the oracle
+    with the armed path always taken ("on": every gap qualifies, the kernel lives 1 s), always
+    expiring ("expire": 1 us lifetime), and off."""
     import torch
     from paper_1909_11150_b200 import GR_F16, Context
     from tests.parity_lib import run_case_on_rank, run_drain_case_on_rank
-    monkeypatch.setenv("GR_ARM", arm)
+    monkeypatch.setenv("GR_ARM", "0" if arm == "off" else "1")
+    monkeypatch.setenv("GR_ARM_GAP_US", "1000000000")
+    monkeypatch.setenv("GR_ARM_US", "1" if arm == "expire" else "1000000")
     base = cfg1_case(11)
     ctx = Context(rank=0, world_size=1, device=0, numel=base.numel, group_of=base.group_of, buffer_dtype=GR_F16,
                   timeout_ms=10000)
@@ -467,8 +471,8 @@ def test_armed_cycles_n1(gpu, arm, monkeypatch):
             else:
                 run_case_on_rank(ctx, case, 0, 100 + seed, gpu, True)
         st = ctx.stats()
-        if arm == "1":
-            assert st.armed_cycles > 0 and st.armed_cycles < st.cycles
+        if arm == "on":
+            assert 0 < st.armed_cycles < st.cycles
         else:
             assert st.armed_cycles == 0
     finally:
