@@ -165,12 +165,16 @@ struct DataParams {
 // launch on the cycle's critical path. The kernel takes the static BvParams from its launch and
 // these per-cycle fields from the descriptor (one PCIe read). skip = 1 retires it unused.
 struct CycleDesc {
-    uint32_t doorbell;               // = the armed kernel's sequence number: run
-    uint32_t skip;                   // 1: exit at once (the host needs the stream back)
-    uint32_t epoch, tag, htag;
-    int32_t parity, new_step, check_async, abort_flag, shutdown_flag, slot, pad;
-    uint32_t bits[GR_BV_INLINE_WORDS];
-    uint32_t marked[GR_BV_INLINE_WORDS];
+    // LL words: (armed kernel's sequence number << 32) | value. Each word validates itself, so
+    // the kernel reads the whole cycle in one PCIe round trip; the host writes word D_CTRL last.
+    uint64_t w[16 + 2 * GR_BV_INLINE_WORDS];
+};
+enum DescWord {
+    D_CTRL = 0,      // bit 0: skip (retire unused); the doorbell is this word carrying seq
+    D_EPOCH = 1, D_TAG = 2, D_HTAG = 3, D_PARITY = 4, D_NEW_STEP = 5, D_CHECK_ASYNC = 6,
+    D_ABORT = 7, D_SHUTDOWN = 8, D_SLOT = 9,
+    D_BITS = 16,                          // [W] host mark bits
+    D_MARKED = 16 + GR_BV_INLINE_WORDS,   // [W] marks taken by the snapshot
 };
 
 // Virtual ranks (gr_init_virtual): every rank's parameters for one launch on one device.

@@ -49,6 +49,11 @@ __device__ __forceinline__ uint32_t ld_relaxed_sys32(const uint32_t *p) {
     asm volatile("ld.relaxed.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
 }
+__device__ __forceinline__ uint64_t ld_acquire_sys64(const uint64_t *p) {
+    uint64_t v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
 __device__ __forceinline__ uint64_t ld_relaxed_sys64(const uint64_t *p) {
     uint64_t v;
     asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
@@ -369,68 +374,70 @@ __global__ void __launch_bounds__(NT, 1024 / NT) bitvector_kernel(const __grid_c
     bitvector_body<NT>(p);
 }
 
-// Armed cycle: launched right after a cycle, before the next one exists. Thread 0 polls the
-// pinned descriptor's doorbell for at most `expire_ns` (bounded residency: one small CTA, and
-// a device-wide synchronize waits at most that long); it acknowledges in pinned memory —
-// ack = seq << 1 | 1 "accepted, running this cycle" or seq << 1 "expired / retired unused" —
-// and the per-cycle fields then come from the descriptor (one PCIe read).
+// Armed cycle: launched right after a cycle, before the next one exists. Its threads poll the
+// pinned descriptor's LL words in parallel (thread i: word i) for at most `expire_ns` (bounded
+// residency: one small CTA; a device-wide synchronize waits at most that long), so the whole
+// cycle arrives in one PCIe round trip after the host writes it. Thread 0 owns the control word
+// and acknowledges in pinned memory: ack = seq << 1 | 1 "accepted, running this cycle", or
+// seq << 1 "expired before the doorbell" (the host then launches the cycle itself).
 template <int NT>
 __global__ void __launch_bounds__(NT, 1024 / NT) bitvector_kernel_armed(const __grid_constant__ BvParams p,
                                                                         const CycleDesc *desc, uint32_t seq,
                                                                         uint64_t expire_ns, uint32_t *ack) {
     __shared__ BvParams sp;
-    __shared__ int s_go;
-    auto rd = [](const void *a) { return ld_relaxed_sys32(reinterpret_cast<const uint32_t *>(a)); };
-    const CycleDesc *d = desc;
-    if (threadIdx.x == 0) {
+    __shared__ volatile int s_state;  // 0 polling, 1 run, 2 leave
+    __shared__ uint32_t sv[16 + 2 * GR_BV_INLINE_WORDS];
+    const int t = threadIdx.x;
+    const bool mine = t < D_SLOT + 1 || (t >= D_BITS && t < D_BITS + p.W) || (t >= D_MARKED && t < D_MARKED + p.W);
+    if (t == 0) s_state = 0;
+    __syncthreads();
+    if (t == 0) {
         const uint64_t dl = globaltimer() + expire_ns;
-        int go = 0;
         for (;;) {
-            if (ld_acquire_sys(&d->doorbell) == seq) {  // rung (skip = retired by the host)
-                go = rd(&d->skip) ? 0 : 1;
-                if (go) st_relaxed_sys32(ack, (seq << 1) | 1u);
+            const uint64_t v = ld_acquire_sys64(&desc->w[D_CTRL]);
+            if ((uint32_t)(v >> 32) == seq) {
+                if (v & 1ull) { s_state = 2; break; }  // retired by the host
+                sv[D_CTRL] = (uint32_t)v;
+                st_relaxed_sys32(ack, (seq << 1) | 1u);
+                s_state = 1;
                 break;
             }
-            if (globaltimer() > dl) {  // nobody came: tell the host to launch this cycle itself
-                fence_acq_rel_sys();
+            if (globaltimer() > dl) {
                 st_relaxed_sys32(ack, seq << 1);
+                s_state = 2;
                 break;
             }
-            __nanosleep(128);
+            __nanosleep(64);
         }
-        s_go = go;
+    } else if (mine) {  // data words: valid once they carry seq (written before the control word)
+        for (;;) {
+            const uint64_t v = ld_relaxed_sys64(&desc->w[t]);
+            if ((uint32_t)(v >> 32) == seq) { sv[t] = (uint32_t)v; break; }
+            if (s_state == 2) break;
+            __nanosleep(64);
+        }
     }
     {   // static part: copy the launch parameters word by word
         const uint32_t *src = reinterpret_cast<const uint32_t *>(&p);
         uint32_t *dst = reinterpret_cast<uint32_t *>(&sp);
-        for (int i = threadIdx.x; i < (int)(sizeof(BvParams) / 4); i += blockDim.x) dst[i] = src[i];
+        for (int i = t; i < (int)(sizeof(BvParams) / 4); i += blockDim.x) dst[i] = src[i];
     }
     __syncthreads();
-    if (!s_go) return;
-    // the descriptor in ONE PCIe round trip: every thread reads one word of it
-    __shared__ CycleDesc sd;
-    {
-        constexpr int HW = (int)(offsetof(CycleDesc, bits) / 4);  // header words, then bits[], marked[]
-        const uint32_t *src = reinterpret_cast<const uint32_t *>(d);
-        uint32_t *dst = reinterpret_cast<uint32_t *>(&sd);
-        for (int i = threadIdx.x; i < HW + 2 * GR_BV_INLINE_WORDS; i += blockDim.x)
-            if (i < HW || (i - HW) % GR_BV_INLINE_WORDS < p.W) dst[i] = rd(src + i);
+    if (s_state != 1) return;
+    for (int w = t; w < p.W; w += blockDim.x) {
+        sp.inline_bits[w] = sv[D_BITS + w];
+        sp.inline_marked[w] = sv[D_MARKED + w];
     }
-    __syncthreads();
-    for (int w = threadIdx.x; w < p.W; w += blockDim.x) {
-        sp.inline_bits[w] = sd.bits[w];
-        sp.inline_marked[w] = sd.marked[w];
-    }
-    if (threadIdx.x == 0) {
-        const int slot = sd.slot;
-        sp.epoch = sd.epoch;
-        sp.tag = sd.tag;
-        sp.htag = sd.htag;
-        sp.parity = sd.parity;
-        sp.new_step = sd.new_step;
-        sp.check_async = sd.check_async;
-        sp.abort_flag = sd.abort_flag;
-        sp.shutdown_flag = sd.shutdown_flag;
+    if (t == 0) {
+        const int slot = (int)sv[D_SLOT];
+        sp.epoch = sv[D_EPOCH];
+        sp.tag = sv[D_TAG];
+        sp.htag = sv[D_HTAG];
+        sp.parity = (int32_t)sv[D_PARITY];
+        sp.new_step = (int32_t)sv[D_NEW_STEP];
+        sp.check_async = (int32_t)sv[D_CHECK_ASYNC];
+        sp.abort_flag = (int32_t)sv[D_ABORT];
+        sp.shutdown_flag = (int32_t)sv[D_SHUTDOWN];
         sp.out_released = p.out_released + (size_t)slot * p.G;
         sp.out_cum = p.out_cum + (size_t)slot * (p.G + 1);
         sp.out_subcum = p.out_subcum + (size_t)slot * (p.G + 1);
@@ -891,11 +898,6 @@ __device__ __forceinline__ bool mbar_test(uint64_t *b, uint32_t parity) {
     return done != 0;
 }
 
-__device__ __forceinline__ uint64_t ld_acquire_sys64(const uint64_t *p) {
-    uint64_t v;
-    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-    return v;
-}
 // progress word of this step: epoch in the high half, elements done (absolute fusion-buffer
 // index of the end of the finished prefix of the chunk) in the low half
 __device__ __forceinline__ uint64_t progress_word(uint32_t epoch, int64_t done) {

@@ -92,6 +92,7 @@ struct gr_ctx {
     int64_t chunk_elems = 0;  // 0 = adaptive per group
     int64_t chunk_target_div = 148, chunk_max = 131072;  // adaptive rule (GR_CHUNK_DIV / GR_CHUNK_MAX)
     int64_t chunk_target_div_fine = 148;                  // fine chunking (N x 148; GR_CHUNK_DIV_FINE)
+    int64_t fine_head = 0;                                // leading quarter-size fine chunks (GR_FINE_HEAD)
     int64_t one_shot_max_bytes = 0;
     uint64_t hash = 0;
 
@@ -416,8 +417,14 @@ int build_layouts(gr_ctx *c, const gr_tensor *table, const int32_t *group_of) {
                 cg = pass ? 16384 : 8192;
                 while (cg * 2 <= target && cg < c->chunk_max) cg *= 2;
             }
-            for (int64_t cb = gbeg[g]; cb < gend[g]; cb += cg) {
-                const int64_t ce = std::min(gend[g], cb + cg);
+            // fine chunking: optionally a head of smaller chunks (GR_FINE_HEAD of them, 1/4 size),
+            // so the first packs of a group released alone finish early (fill of the pipeline)
+            int64_t nsmall = (pass == 1) ? c->fine_head : 0;
+            const int64_t csmall = std::max<int64_t>(8192, cg / 4 / 8 * 8);
+            for (int64_t cb = gbeg[g]; cb < gend[g];) {
+                const int64_t step = (nsmall > 0 && csmall < cg) ? csmall : cg;
+                if (nsmall > 0) --nsmall;
+                const int64_t ce = std::min(gend[g], cb + step);
                 Chunk ch;
                 ch.seg_begin = (int32_t)c->segs.size();
                 for (int32_t q = pos0; q < pos; ++q) {
@@ -437,6 +444,7 @@ int build_layouts(gr_ctx *c, const gr_tensor *table, const int32_t *group_of) {
                 c->chunks.push_back(ch);
                 c->chunk_begin.push_back(cb);
                 c->chunk_end.push_back(ce);
+                cb = ce;
             }
             gnc[g] = (int32_t)c->chunks.size() - gcb[g];
         }
@@ -476,6 +484,7 @@ int build_layouts(gr_ctx *c, const gr_tensor *table, const int32_t *group_of) {
     h = fnv1a(h, &c->world.comm_ctas, sizeof c->world.comm_ctas);  // sets the default lags (x grid)
     h = fnv1a(h, &c->chunk_target_div, sizeof c->chunk_target_div);
     h = fnv1a(h, &c->chunk_target_div_fine, sizeof c->chunk_target_div_fine);
+    h = fnv1a(h, &c->fine_head, sizeof c->fine_head);
     h = fnv1a(h, &c->chunk_max, sizeof c->chunk_max);
     h = fnv1a(h, c->numel.data(), sizeof(int64_t) * T);
     h = fnv1a(h, c->grad_f16.data(), sizeof(int32_t) * T);
@@ -780,8 +789,7 @@ int arm(gr_ctx *c) {
 void disarm(gr_ctx *c) {
     if (!c->armed) return;
     gr::CycleDesc *h = c->h_desc + c->arm_seq % kArmSlots;
-    h->skip = 1;
-    __atomic_store_n(&h->doorbell, c->arm_seq, __ATOMIC_RELEASE);
+    __atomic_store_n(&h->w[gr::D_CTRL], ((uint64_t)c->arm_seq << 32) | 1ull, __ATOMIC_RELEASE);  // skip
     c->armed = false;
 }
 
@@ -967,6 +975,7 @@ static int create_ctx(gr_ctx **out, const gr_world *world, const gr_tensor *tabl
     c->chunk_target_div_fine = 148 * (int64_t)std::max(1, world->world_size);
     if (const char *cd = getenv("GR_CHUNK_DIV")) c->chunk_target_div = std::max<int64_t>(1, atoll(cd));  // tuning
     if (const char *cf = getenv("GR_CHUNK_DIV_FINE")) c->chunk_target_div_fine = std::max<int64_t>(1, atoll(cf));
+    if (const char *fh = getenv("GR_FINE_HEAD")) c->fine_head = std::max<int64_t>(0, atoll(fh));
     if (const char *cm = getenv("GR_CHUNK_MAX")) c->chunk_max = std::max<int64_t>(8192, atoll(cm));      // tuning
     if (world->chunk_elems == 0)
         if (const char *ce = getenv("GR_CHUNK_ELEMS")) c->chunk_elems = std::max<int64_t>(8, atoll(ce) / 8 * 8);  // tuning
@@ -1256,9 +1265,14 @@ static int step_impl(gr_ctx *c, int32_t *released, gr_cycle_info *info, uint32_t
         step_fresh = c->step_fresh;
         c->step_fresh = false;
         async_used = c->async_used;
-        if (hd) {        // ... in the armed kernel's pinned descriptor
-            memcpy(hd->bits, c->h_bits, sizeof(uint32_t) * c->W);
-            memcpy(hd->marked, c->h_marked, sizeof(uint32_t) * c->W);
+        if (hd) {        // ... in the armed kernel's pinned descriptor (LL words, this seq)
+            const uint64_t sq = (uint64_t)c->arm_seq << 32;
+            for (int w = 0; w < c->W; ++w) {
+                hd->w[gr::D_BITS + w] = sq | c->h_bits[w];
+                hd->w[gr::D_MARKED + w] = sq | c->h_marked[w];
+                p.inline_bits[w] = c->h_bits[w];      // kept for a fallback launch
+                p.inline_marked[w] = c->h_marked[w];
+            }
         } else if (p_inline) {  // the mark bits travel in the launch parameters
             memcpy(p.inline_bits, c->h_bits, sizeof(uint32_t) * c->W);
             memcpy(p.inline_marked, c->h_marked, sizeof(uint32_t) * c->W);
@@ -1334,18 +1348,18 @@ static int step_impl(gr_ctx *c, int32_t *released, gr_cycle_info *info, uint32_t
         CK(c, cudaMemcpyAsync(c->d_hbits_dev, bits_stage, sizeof(uint32_t) * 2 * c->W, cudaMemcpyHostToDevice,
                               c->s_coord));
     bool ran_armed = false;
-    if (hd) {  // ring the armed kernel: the descriptor first, the doorbell last (x86 keeps store order)
-        hd->skip = 0;
-        hd->epoch = p.epoch;
-        hd->tag = p.tag;
-        hd->htag = p.htag;
-        hd->parity = p.parity;
-        hd->new_step = p.new_step;
-        hd->check_async = p.check_async;
-        hd->abort_flag = p.abort_flag;
-        hd->shutdown_flag = p.shutdown_flag;
-        hd->slot = slot;
-        __atomic_store_n(&hd->doorbell, c->arm_seq, __ATOMIC_RELEASE);
+    if (hd) {  // ring the armed kernel: the data words first, the control word last (x86 keeps store order)
+        const uint64_t sq = (uint64_t)c->arm_seq << 32;
+        hd->w[gr::D_EPOCH] = sq | p.epoch;
+        hd->w[gr::D_TAG] = sq | p.tag;
+        hd->w[gr::D_HTAG] = sq | p.htag;
+        hd->w[gr::D_PARITY] = sq | (uint32_t)p.parity;
+        hd->w[gr::D_NEW_STEP] = sq | (uint32_t)p.new_step;
+        hd->w[gr::D_CHECK_ASYNC] = sq | (uint32_t)p.check_async;
+        hd->w[gr::D_ABORT] = sq | (uint32_t)p.abort_flag;
+        hd->w[gr::D_SHUTDOWN] = sq | (uint32_t)p.shutdown_flag;
+        hd->w[gr::D_SLOT] = sq | (uint32_t)slot;
+        __atomic_store_n(&hd->w[gr::D_CTRL], sq, __ATOMIC_RELEASE);
         c->armed = false;
         // rung well inside the kernel's lifetime (which starts after its launch): it cannot have
         // expired, go on. Otherwise its acknowledgement tells: accepted, or expired before the
@@ -1363,10 +1377,7 @@ static int step_impl(gr_ctx *c, int32_t *released, gr_cycle_info *info, uint32_t
         if (a & 1u) {
             ran_armed = true;
             c->stats.armed_cycles++;
-        } else {  // expired: this cycle's marks travel in the launch parameters after all
-            memcpy(p.inline_bits, hd->bits, sizeof(uint32_t) * c->W);
-            memcpy(p.inline_marked, hd->marked, sizeof(uint32_t) * c->W);
-        }
+        }  // else expired: the cycle's marks are in p.inline_* for the launch below
     }
     if (ran_armed) {
     } else if (c->vg) {

@@ -1,5 +1,5 @@
 # r02 call q (1 GPU): bounded armed kernels — correctness first, then cycle latency
-P=gpurun_out/r19
+P=gpurun_out/r20
 python -c "import __graft_entry__ as g; g.build()" > ${P}_build.log 2>&1
 timeout 600 python -m pytest tests/test_gpu_parity.py -m gpu -x -q -k "armed or cfg1_n1 or same_context or async or drain or racing or released" > ${P}_pytest_arm.log 2>&1; prc=$?; echo "pytest arm rc $prc"; tail -3 ${P}_pytest_arm.log
 if [ $prc -ne 0 ]; then exit 1; fi
@@ -7,8 +7,8 @@ for A in 1 0; do
   GR_ARM=$A timeout 120 python tools/bench_cycle.py --iters 3000 | sed "s/^/GR_ARM=$A /" >> ${P}_cycle.txt 2>&1
   GR_ARM=$A timeout 120 python tools/bench_cycle.py --iters 3000 --release | sed "s/^/GR_ARM=$A /" >> ${P}_cycle.txt 2>&1
 done
-GR_TRACE=gpurun_out/trc4 GR_TRACE_MAX_CYCLES=2000 timeout 120 python tools/bench_cycle.py --iters 1500 >> ${P}_cycle.txt 2>&1
-python tools/trace_summary.py gpurun_out/trc4 2>&1 | head -4 >> ${P}_cycle.txt
+GR_TRACE=gpurun_out/trc5 GR_TRACE_MAX_CYCLES=2000 timeout 120 python tools/bench_cycle.py --iters 1500 >> ${P}_cycle.txt 2>&1
+python tools/trace_summary.py gpurun_out/trc5 2>&1 | head -4 >> ${P}_cycle.txt
 cat ${P}_cycle.txt
 timeout 1500 python -m pytest tests -m gpu -x -q > ${P}_pytest_all.log 2>&1; echo "pytest all rc $?"; tail -2 ${P}_pytest_all.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > ${P}_smoke.log 2>&1; echo "smoke rc $?"
