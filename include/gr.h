@@ -70,7 +70,7 @@ typedef struct {
     gr_dtype buffer_dtype;      /* fusion-buffer (wire) precision: GR_F16 or GR_F32 */
     int64_t one_shot_max_bytes; /* messages up to this many buffer bytes use the one-shot
                                    reduce, larger ones the two-shot (or NVLS); -1 = library
-                                   default: 128 MiB at N=2, 32 MiB at N=3, 8 MiB at N=4,
+                                   default: 128 MiB at N=2, 32 MiB at N=3, 4 MiB at N=4,
                                    1 MiB above (measured crossovers) */
     int32_t timeout_ms;         /* bound on any cross-rank wait; 0 = 20000 */
     int32_t comm_ctas;          /* CTAs of the fused reduce kernel; 0 = library default */

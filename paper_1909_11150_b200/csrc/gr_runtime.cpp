@@ -984,7 +984,8 @@ static int create_ctx(gr_ctx **out, const gr_world *world, const gr_tensor *tabl
     // local HBM traffic. Crossover measured with tools/bench_cfg5.py (profiles/r01_cfg):
     // N=2 between 128 and 256 MiB, N=4 at ~8 MiB; N>=8 reads 7 peer copies, kept at 1 MiB.
     {
-        const int64_t thr = c->N <= 2 ? (128ll << 20) : c->N == 3 ? (32ll << 20) : c->N == 4 ? (8ll << 20) : (1ll << 20);
+        // (round 2, N=4: two-shot 64.7 vs one-shot 69.3 us at 8 MiB, equal at 4 MiB: threshold 4 MiB)
+        const int64_t thr = c->N <= 2 ? (128ll << 20) : c->N == 3 ? (32ll << 20) : c->N == 4 ? (4ll << 20) : (1ll << 20);
         c->one_shot_max_bytes = world->one_shot_max_bytes >= 0 ? world->one_shot_max_bytes : thr;
     }
     // knobs that fix the cross-rank queue order / algorithm: read before the table hash so every
