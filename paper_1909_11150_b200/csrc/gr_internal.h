@@ -134,6 +134,9 @@ struct DataParams {
     uint64_t *pack_flag[GR_MAX_RANKS]; // every rank's pack progress [C][N] for this parity
     uint64_t *rs_flag[GR_MAX_RANKS];   // every rank's reduce-scatter progress [C] for this parity
     int32_t *work_counter;             // device, reset by the last CTA
+    int32_t *pack_counter;             // device: the PACK queue of queue_mode 1, reset by the last CTA
+    int32_t queue_mode;                // 0: triples {PACK, RS, AG} with lags; 1: split PACK / dependent queues
+    int32_t lagd;                      // queue_mode 1: all-gather lag in dependent positions
     int32_t *done_counter;
     volatile int32_t *abort_dev;       // device flag: bail out (set on timeout)
     HostError *err;                    // host-mapped

@@ -1321,9 +1321,78 @@ __device__ __forceinline__ void xfer_body(const DataParams &p, const int cta, co
             }
             return true;
         };
+        bool ok = true;
+        if (p.queue_mode == 1) {
+            // Split queues (round 2): PACK items (no dependencies) on their own counter; the
+            // dependent queue holds position k = {RS/RED/NRS(k), AG(k - lagd)}. When the next
+            // dependent item's first sub-tile is not ready yet, the producer packs instead of
+            // parking, so reduce-scatters can be claimed early without idling SMs. Deadlock-free:
+            // a producer blocks on a dependency only once every PACK is claimed, and PACK items
+            // never wait; every reduce-scatter depends only on PACKs, every all-gather only on a
+            // reduce-scatter claimed earlier in the dependent queue.
+            const int lagd = p.lagd;
+            const int nd = titems > 0 ? titems + (ALGO == ALGO_ONESHOT ? 0 : lagd) : 0;
+            bool packs_left = titems > 0;
+            auto one_pack = [&]() -> bool {  // false: the pack queue is exhausted
+                for (;;) {
+                    int kp = 0;
+                    if (lane == 0) kp = atomicAdd(p.pack_counter, 1);
+                    kp = __shfl_sync(FULL, kp, 0);
+                    if (kp >= titems) return false;
+                    const int own = kp % p.N;
+                    if (ALGO == ALGO_TWOSHOT && own == p.rank) continue;  // owned chunks are not packed
+                    if (p.trace && lane == 0) { const uint64_t t = globaltimer(); p.trace[(size_t)kp * 4] = t; p.trace[(size_t)kp * 4 + 1] = t; }
+                    produce(K_PACK, kp, chunk_of(kp), p.sub_pack, 0, -1, true, nullptr, 0, 0u, 0, nullptr, own);
+                    return true;
+                }
+            };
+            // is the first sub-tile of an item ready (one read of each progress word, no wait)?
+            auto ready_now = [&](const uint64_t *wbase, int wstride, unsigned wmask, int c, int64_t sub) -> bool {
+                bool r = true;
+                if ((wmask >> lane) & 1u) {
+                    const int64_t cb = p.chunk_begin[c], ce = p.chunk_end[c];
+                    const int64_t need = (cb + sub < ce) ? cb + sub : ce;
+                    const uint64_t v = ld_acquire_sys64(wbase + (size_t)lane * wstride);
+                    r = (uint32_t)(v >> 32) == p.epoch && (uint32_t)v >= (uint32_t)need;
+                }
+                return __all_sync(FULL, r);
+            };
+            const unsigned all = (1u << p.N) - 1u;
+            const unsigned wm_red = ALGO == ALGO_TWOSHOT ? all & ~(1u << p.rank) : all;
+            for (;;) {
+                int kd = 0;
+                if (lane == 0) kd = atomicAdd(p.work_counter, 1);
+                kd = __shfl_sync(FULL, kd, 0);
+                if (kd >= nd || !ok) break;
+                if (p.dbg && lane == 0) p.dbg[(size_t)cta * 8] = (uint64_t)kd;
+                if (kd < titems && (ALGO == ALGO_ONESHOT || kd % p.N == p.rank)) {
+                    const int c = chunk_of(kd), own = kd % p.N;
+                    const uint64_t *wb = p.pack_flag[p.rank] + (size_t)c * p.N;
+                    const int64_t sub = ALGO == ALGO_NVLS ? ((int64_t)1 << 30) : p.sub_red;
+                    while (packs_left && !ready_now(wb, 1, wm_red, c, sub)) packs_left = one_pack();
+                    uint64_t *tr = p.trace ? p.trace + ((size_t)tstride + kd) * 4 : nullptr;
+                    if (tr && lane == 0) tr[0] = globaltimer();
+                    if (ALGO == ALGO_NVLS) ok = produce(K_NRS, tstride + kd, c, 1 << 30, 0, -1, false, wb, 1, wm_red, 1, tr, own);
+                    else ok = produce(ALGO == ALGO_ONESHOT ? K_RED : K_RS, tstride + kd, c, p.sub_red, 1, -1, true, wb, 1, wm_red, 1, tr, own);
+                    if (!ok) break;
+                }
+                const int i2 = kd - lagd;
+                if (ALGO != ALGO_ONESHOT && i2 >= 0 && i2 < titems && i2 % p.N != p.rank) {
+                    const int c = chunk_of(i2), owner = i2 % p.N;
+                    const uint64_t *wb = p.rs_flag[p.rank] + c;
+                    const unsigned wm = 1u << (ALGO == ALGO_NVLS ? 0 : owner);
+                    while (packs_left && !ready_now(wb, 0, wm, c, p.sub_ag)) packs_left = one_pack();
+                    uint64_t *tr = p.trace ? p.trace + ((size_t)2 * tstride + i2) * 4 : nullptr;
+                    if (tr && lane == 0) tr[0] = globaltimer();
+                    ok = produce(K_AG, 2 * tstride + i2, c, p.sub_ag, ALGO == ALGO_NVLS ? 3 : 2, owner, false, wb, 0, wm, 2,
+                                 tr, owner);
+                    if (!ok) break;
+                }
+            }
+            while (ok && packs_left) packs_left = one_pack();  // every CTA helps finish the packs
+        } else {
         int kq = 0;
         if (lane == 0) kq = atomicAdd(p.work_counter, 1);
-        bool ok = true;
         for (;;) {
             const int k = __shfl_sync(FULL, kq, 0);
             if (k >= nk || !ok) break;
@@ -1376,6 +1445,7 @@ __device__ __forceinline__ void xfer_body(const DataParams &p, const int cta, co
                 }
             }
         }
+        }  // triple queue
         // flag waits are spread over the polling lanes: report the largest
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
@@ -1617,6 +1687,7 @@ __device__ __forceinline__ void xfer_body(const DataParams &p, const int cta, co
         __threadfence();
         if (atomicAdd(p.done_counter, 1) == nctas - 1) {
             *p.work_counter = 0;
+            *p.pack_counter = 0;
             *p.done_counter = 0;
             __threadfence();
         }

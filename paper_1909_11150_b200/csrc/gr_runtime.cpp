@@ -178,6 +178,7 @@ struct gr_ctx {
     int data_ctas[4] = {0, 0, 0, 0};       // world.comm_ctas (or every SM)
     int data_ctas_full[4] = {0, 0, 0, 0};  // every SM (drain cycles)
     int lag1 = -1, lag2 = -1;  // GR_LAG1 / GR_LAG2 overrides (tuning; -1 = default multiple of the grid)
+    int queue_mode = 0, lagd = -1;  // GR_QUEUE (0 triples, 1 split PACK / dependent queues), GR_LAGD
     // TMA stage ring of the xfer kernel: 2 x 96 KB (measured against 4 x 48 / 3 x 64 / 6 x 32 /
     // 8 x 24 KB: per-stage fixed costs make small stages slow — 0.88 vs 0.81 of HBM peak on
     // virtual ranks, 2-5% at N = 2/4, profiles/r02/virtual_chunk_stage_sweep.txt)
@@ -481,6 +482,8 @@ int build_layouts(gr_ctx *c, const gr_tensor *table, const int32_t *group_of) {
     h = fnv1a(h, &c->lag1, sizeof c->lag1);
     h = fnv1a(h, &c->lag2, sizeof c->lag2);
     h = fnv1a(h, &c->fine_below, sizeof c->fine_below);
+    h = fnv1a(h, &c->queue_mode, sizeof c->queue_mode);
+    h = fnv1a(h, &c->lagd, sizeof c->lagd);
     h = fnv1a(h, &c->world.comm_ctas, sizeof c->world.comm_ctas);  // sets the default lags (x grid)
     h = fnv1a(h, &c->chunk_target_div, sizeof c->chunk_target_div);
     h = fnv1a(h, &c->chunk_target_div_fine, sizeof c->chunk_target_div_fine);
@@ -1000,6 +1003,8 @@ static int create_ctx(gr_ctx **out, const gr_world *world, const gr_tensor *tabl
         return fail(nullptr, GR_EINVAL, "GR_LAG2 (%s) must exceed GR_LAG1 (%s)", getenv("GR_LAG2"), getenv("GR_LAG1"));
     }
     if (const char *fb = getenv("GR_FINE_BELOW")) c->fine_below = std::max(0, atoi(fb));
+    if (const char *qm = getenv("GR_QUEUE")) c->queue_mode = atoi(qm) == 1 ? 1 : 0;
+    if (const char *ld = getenv("GR_LAGD")) c->lagd = std::max(1, atoi(ld));
     c->dry = world->device < 0;
     if (c->world.timeout_ms <= 0) c->world.timeout_ms = kDefaultTimeoutMs;
     int rc = build_layouts(c, table, group_of);
@@ -1430,6 +1435,8 @@ static int step_impl(gr_ctx *c, int32_t *released, gr_cycle_info *info, uint32_t
         if (c->d_dbg) CK(c, cudaMemsetAsync(c->d_dbg, 0, sizeof(uint64_t) * 8 * 1024, c->s_data));
         d.work_counter = c->d_counters;
         d.done_counter = c->d_counters + 1;
+        d.pack_counter = c->d_counters + 3;
+        d.queue_mode = c->queue_mode;
         d.abort_dev = c->d_counters + 2;
         d.err = c->d_err;
         d.trace = c->d_trace ? c->d_trace + (size_t)slot * c->trace_slot_u64 : nullptr;
@@ -1473,6 +1480,7 @@ static int step_impl(gr_ctx *c, int32_t *released, gr_cycle_info *info, uint32_t
         d.lag1 = c->lag1 >= 0 ? c->lag1 : 3 * ctas;
         d.lag2 = c->lag2 >= 0 ? c->lag2 : 8 * ctas;
         if (d.lag2 <= d.lag1) d.lag2 = d.lag1 + ctas;  // one override against the other's default
+        d.lagd = c->lagd >= 0 ? c->lagd : 2 * ctas;
         CK(c, cudaEventRecord(c->ev_bv, c->s_coord));
         CK(c, cudaStreamWaitEvent(c->s_data, c->ev_bv, 0));
         std::pair<cudaEvent_t, cudaEvent_t> evd{};

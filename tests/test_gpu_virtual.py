@@ -239,6 +239,39 @@ def test_virtual_push_numeric_edges_stats_steps(gpu, n, push_mode):
     run_virtual_case(Case(n, f.numel, f.group_of, mark, 60 + n), 60 + n, gpu, True, one_shot_max_bytes=TWO_SHOT)
 
 
+# ------------------------------------------------------------------ split queues (GR_QUEUE=1)
+
+@pytest.mark.parametrize("n", [2, 3, 4, 8])
+def test_virtual_split_queue(gpu, n, monkeypatch):
+    """Split PACK / dependent queues: a producer packs while its next
+    reduce-scatter / all-gather is not ready. Ragged sizes and both algorithms forced, fp16
+    gradients, integer payloads, cfg1 schedules, the fcn220m set — bit-exact against
+    oracle.emulate, replicas identical."""
+    from paper_1909_11150_b200 import GR_ALGO_ONESHOT, GR_ALGO_TWOSHOT
+    from tests.parity_lib import run_virtual_case
+    monkeypatch.setenv("GR_QUEUE", "1")
+    for seed in range(2):
+        rng = np.random.default_rng(200 + seed)
+        T = int(rng.integers(1, 24))
+        G = int(rng.integers(1, T + 1))
+        numel = rng.integers(1, 200000, size=T).astype(np.int64)
+        case = Case(n, numel, random_partition(T, G, rng), random_mark_schedule(n, T, seed, 3), seed)
+        gf = (rng.random(T) < 0.3).tolist()
+        for buf16 in (True, False):
+            chunk = int(rng.choice([1024, 4096, 32768]))
+            out = run_virtual_case(case, seed, gpu, buf16, grad_f16=gf, chunk_elems=chunk, one_shot_max_bytes=TWO_SHOT)
+            assert _algos(out) == {GR_ALGO_TWOSHOT}
+            out = run_virtual_case(case, seed, gpu, buf16, grad_f16=gf, chunk_elems=chunk, one_shot_max_bytes=ONE_SHOT)
+            assert _algos(out) == {GR_ALGO_ONESHOT}
+        run_virtual_case(case, seed, gpu, True, kind="int", one_shot_max_bytes=TWO_SHOT)
+    for seed in range(3):
+        run_virtual_case(cfg1_case(seed, N=n), seed, gpu, seed % 2 == 0, timeout_ms=20000)
+    if n in (2, 4):
+        f = fcn220m()
+        mark = reverse_layer_schedule(len(f.layers), n, f.release_order, layers_per_cycle=1, jitter_seed=n, max_shift=2)
+        run_virtual_case(Case(n, f.numel, f.group_of, mark, 70 + n), 70 + n, gpu, True, one_shot_max_bytes=TWO_SHOT)
+
+
 # ------------------------------------------------------------------ failure paths (§8(b) errors)
 
 def _tiny_world(n, **kw):
