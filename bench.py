@@ -492,7 +492,7 @@ def main():
                "wait": "gr_wait_async (stream-ordered; the production contract)",
                "ms_per_step_blocking_wait": round(ms_blocking, 4),
                "gpu_launches": launches, "launches_per_step": launches / args.steps,
-               "armed_cycles": int(st.armed_cycles),
+               "armed_cycles": int(st.armed_cycles), "armed_expired": int(st.armed_expired),
                "bitvector_kernel_us": round(bv_ms * 1e3, 2),
                "roofline": roof, "clocks": clk.summary(), "e2e": e2e, "cpu_baseline": cpu}
         if nvlink is not None:

@@ -288,6 +288,8 @@ typedef struct {
                                       on this rank, so none could be released on any rank */
     int64_t armed_cycles;       /* cycles run by an armed bitvector kernel (launched ahead of the
                                    cycle, rung through a pinned doorbell; see gr_step) */
+    int64_t armed_expired;      /* cycles whose armed kernel had expired before its doorbell (the
+                                   cycle was launched as usual) */
 } gr_stats;
 
 int gr_query(gr_ctx *ctx, int32_t kind, void *out, size_t bytes);

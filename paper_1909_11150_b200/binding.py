@@ -48,7 +48,7 @@ class GrStats(ctypes.Structure):
                 ("data_kernel_ms", ctypes.c_double), ("bitvector_kernel_ms", ctypes.c_double),
                 ("host_step_us", ctypes.c_double), ("host_wait_us", ctypes.c_double),
                 ("bitvector_device_us", ctypes.c_double), ("data_launches_skipped", ctypes.c_int64),
-                ("armed_cycles", ctypes.c_int64)]
+                ("armed_cycles", ctypes.c_int64), ("armed_expired", ctypes.c_int64)]
 
 
 class GrError(RuntimeError):

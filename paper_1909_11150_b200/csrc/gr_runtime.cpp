@@ -1383,6 +1383,8 @@ static int step_impl(gr_ctx *c, int32_t *released, gr_cycle_info *info, uint32_t
         if (a & 1u) {
             ran_armed = true;
             c->stats.armed_cycles++;
+        } else {
+            c->stats.armed_expired++;
         }  // else expired: the cycle's marks are in p.inline_* for the launch below
     }
     if (ran_armed) {

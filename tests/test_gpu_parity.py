@@ -472,9 +472,11 @@ def test_armed_cycles_n1(gpu, arm, monkeypatch):
                 run_case_on_rank(ctx, case, 0, 100 + seed, gpu, True)
         st = ctx.stats()
         if arm == "on":
-            assert 0 < st.armed_cycles < st.cycles
+            assert 0 < st.armed_cycles < st.cycles and st.armed_expired == 0
+        elif arm == "expire":  # a 1 us lifetime: most armed kernels expire, a few are rung in time
+            assert st.armed_expired > 0 and st.armed_cycles + st.armed_expired < st.cycles
         else:
-            assert st.armed_cycles == 0
+            assert st.armed_cycles == 0 and st.armed_expired == 0
     finally:
         ctx.gr_finalize()
 
