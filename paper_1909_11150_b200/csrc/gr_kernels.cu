@@ -89,8 +89,24 @@ constexpr int BV_BATCH = GR_BV_BATCH;
 // this step, sC[Gw] complete-group bits (Gw = ceil(G/32)).
 // Two instantiations: 256 threads (small bitvectors; 56 registers, co-resident with a running
 // reduction) and 1024 threads (W > 64 words, i.e. more than ~2000 tensors).
+// Prologue loads of a cycle: released bits of this step and the group records, into the
+// kernel's shared memory (an armed kernel runs this while it waits for its doorbell).
+__device__ __forceinline__ void bitvector_preload(const BvParams &p) {
+    extern __shared__ uint32_t smem[];
+    const int W = p.W, G = p.G, Gw = (p.G + 31) / 32;
+    uint32_t *sR = smem + 2 * W, *sC = smem + 3 * W;
+    for (int w = threadIdx.x; w < W; w += blockDim.x) sR[w] = p.rel_words[w];
+    for (int i = threadIdx.x; i < Gw; i += blockDim.x) sC[i] = 0u;
+    if (p.stage_groups) {
+        GroupInfo *sG = reinterpret_cast<GroupInfo *>(smem + ((3 * W + Gw + 1) & ~1));
+        const uint2 *src = reinterpret_cast<const uint2 *>(p.groups);
+        uint2 *dst = reinterpret_cast<uint2 *>(sG);
+        for (int i = threadIdx.x; i < 3 * G; i += blockDim.x) dst[i] = src[i];
+    }
+}
+
 template <int NT>
-__device__ __forceinline__ void bitvector_body(const BvParams &p) {
+__device__ __forceinline__ void bitvector_body(const BvParams &p, bool preloaded = false) {
     extern __shared__ uint32_t smem[];
     const int W = p.W, G = p.G, Gw = (p.G + 31) / 32;
     uint32_t *sL = smem, *sA = smem + W, *sR = smem + 2 * W, *sC = smem + 3 * W;
@@ -105,16 +121,11 @@ __device__ __forceinline__ void bitvector_body(const BvParams &p) {
     if (tid == 0) { s_timeout = 0; s_elems = 0ull; }
     // released bits of this step (a new step starts from none); the group records are fetched
     // in the same load wave (no dependent global round trips later in the cycle)
-    for (int w = tid; w < W; w += blockDim.x) sR[w] = p.new_step ? 0u : p.rel_words[w];
-    for (int i = tid; i < Gw; i += blockDim.x) sC[i] = 0u;
-    const GroupInfo *gi = p.groups;
-    if (p.stage_groups) {
-        GroupInfo *sG = reinterpret_cast<GroupInfo *>(smem + ((3 * W + Gw + 1) & ~1));
-        const uint2 *src = reinterpret_cast<const uint2 *>(p.groups);
-        uint2 *dst = reinterpret_cast<uint2 *>(sG);
-        for (int i = tid; i < 3 * G; i += blockDim.x) dst[i] = src[i];
-        gi = sG;
-    }
+    const GroupInfo *gi = p.stage_groups ? reinterpret_cast<const GroupInfo *>(smem + ((3 * W + Gw + 1) & ~1))
+                                         : p.groups;
+    if (!preloaded) bitvector_preload(p);
+    if (p.new_step)
+        for (int w = tid; w < W; w += blockDim.x) sR[w] = 0u;
     __syncthreads();
 
     // ---- step 1: populate from pending requests, publish ----
@@ -390,6 +401,9 @@ __global__ void __launch_bounds__(NT, 1024 / NT) bitvector_kernel_armed(const __
     const int t = threadIdx.x;
     const bool mine = t < D_SLOT + 1 || (t >= D_BITS && t < D_BITS + p.W) || (t >= D_MARKED && t < D_MARKED + p.W);
     if (t == 0) s_state = 0;
+    // the previous cycle's kernel finished before this one started (stream order): its released
+    // bits and the static group records can be loaded while the doorbell is still awaited
+    bitvector_preload(p);
     __syncthreads();
     if (t == 0) {
         const uint64_t dl = globaltimer() + expire_ns;
@@ -444,7 +458,7 @@ __global__ void __launch_bounds__(NT, 1024 / NT) bitvector_kernel_armed(const __
         sp.out_info = p.out_info + slot;
     }
     __syncthreads();
-    bitvector_body<NT>(sp);
+    bitvector_body<NT>(sp, true);
 }
 
 template <int NT>
