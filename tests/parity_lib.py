@@ -76,7 +76,10 @@ def check_values(out_np, gs, N, buffer_f16: bool, grad_f16_t: bool, where="", ex
         if o64.size == 0:
             return
     if buffer_f16:
-        tol = 2.0 ** -10 * N * float(np.max(np.abs(stack)))
+        # reading R11: the north-star bound is relative; a tensor whose values all sit in fp16's
+        # subnormal range (|g| < 2^-14) is rounded with an absolute error, so the bound gains the
+        # subnormal quantum 2^-24 (input + output rounding, 2^-25 each)
+        tol = 2.0 ** -10 * N * float(np.max(np.abs(stack))) + 2.0 ** -24
         assert np.all(np.abs(o64 - ref) <= tol), f"{where}: fp16 tolerance violated"
     else:
         bound = 1e-6 * np.maximum(np.abs(ref), np.mean(np.abs(stack), axis=0))
