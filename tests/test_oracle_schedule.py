@@ -146,6 +146,27 @@ def test_permutation_schedules_n2_closed_form(orc):
             assert list(r.rel_cycle) == closed_form(g, m)
 
 
+@pytest.mark.parametrize("N,T", [(2, 6), (3, 4)])
+def test_permutation_schedules_exhaustive(orc, N, T):
+    """V2 exhaustively over permutation readiness (one mark per cycle per rank) for every set
+    partition: rank 0 marks in identity order (any schedule is one of these after relabeling the
+    tensors, and the closed form and the partition set are invariant under relabeling), every
+    other rank in every order — N=2, T=6: 203 x 720 schedules; N=3, T=4: 15 x 24^2."""
+    perms = list(itertools.permutations(range(T)))
+    cases = 0
+    for part in set_partitions(T):
+        g = np.array(part, dtype=np.int32)
+        for rest in itertools.product(perms, repeat=N - 1):
+            m = np.zeros((N, T), dtype=np.int32)
+            m[0] = np.arange(T)
+            for r, pr in enumerate(rest, start=1):
+                m[r, list(pr)] = np.arange(T)
+            res = orc.simulate_step(N, g, m, max_cycles=T + 2)
+            assert res.rc == 0 and list(res.rel_cycle) == closed_form(g, m), (part, rest)
+            cases += 1
+    assert cases == len(list(set_partitions(T))) * len(perms) ** (N - 1)
+
+
 def test_special_cases(orc):
     rng = np.random.default_rng(9)
     T = 12
