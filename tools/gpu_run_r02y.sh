@@ -9,3 +9,4 @@ python tools/trace_summary.py gpurun_out/trc6 2>&1 | head -4 >> ${P}_cycle.txt
 cat ${P}_cycle.txt
 timeout 600 python bench.py > ${P}_bench_n1.log 2>&1; echo "bench rc $?"
 tail -1 ${P}_bench_n1.log | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['ms_per_step'], d['roofline']['frac'], d['cycle_latency_us'], d['ms_per_step_with_grad_stats'], d['e2e']['ms_per_step'], d['gpu_launches'], d.get('armed_cycles'), d.get('armed_expired'))"
+timeout 1000 python tools/stress.py --minutes 12 --seed 2 > ${P}_stress.log 2>&1; echo "stress rc $?"; tail -2 ${P}_stress.log
