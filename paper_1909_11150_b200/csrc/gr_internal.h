@@ -7,6 +7,7 @@
 #define GR_STATUS_BITS 2
 #define GR_SLOT_RING 64            // released-list slots in flight (cycle % ring)
 #define GR_BV_INLINE_WORDS 64      // host mark bits passed as kernel parameters up to this W
+#define GR_ARM_SLOTS 4             // armed-cycle descriptors in flight (cycle sq uses sq % 4)
 
 namespace gr {
 
@@ -54,7 +55,9 @@ struct DevCycle {
     int32_t total_chunks;
     int64_t elems;
     int32_t total_subs;    // local-kernel sub-items of the released groups
-    int32_t pad;
+    uint32_t tag;          // the cycle's hand-off tag, stored last (release): a data kernel that
+                           // is not ordered after the bitvector kernel by a stream event (armed
+                           // cycles) waits for it
 };
 
 // Per-group constants the bitvector kernel needs (one 24-byte record per group, so one load
@@ -160,13 +163,14 @@ struct DataParams {
     uint32_t epoch;
     float inv_n;
     uint64_t timeout_ns;
+    uint32_t wait_tag;                 // != 0: wait until info->tag == wait_tag before reading the cycle
 };
 
-// Armed cycles (one rank per process, W <= GR_BV_INLINE_WORDS, tight cycle loops): right after
-// a cycle the next cycle's bitvector kernel is launched and polls `doorbell` (pinned host
-// memory) for a bounded time; a cycle writes this descriptor and rings the doorbell — no kernel
-// launch on the cycle's critical path. The kernel takes the static BvParams from its launch and
-// these per-cycle fields from the descriptor (one PCIe read). skip = 1 retires it unused.
+// Armed cycles (one rank per process, W <= GR_BV_INLINE_WORDS, tight cycle loops): a bitvector
+// kernel stays resident across cycles, polling the next cycle's descriptor (pinned host memory)
+// for a bounded time; a cycle writes its descriptor and rings the doorbell — no kernel launch on
+// the cycle's critical path. The kernel takes the static BvParams from its launch and the
+// per-cycle fields from the descriptor (one PCIe round trip). skip = 1 retires it.
 struct CycleDesc {
     // LL words: (armed kernel's sequence number << 32) | value. Each word validates itself, so
     // the kernel reads the whole cycle in one PCIe round trip; the host writes word D_CTRL last.
@@ -195,9 +199,10 @@ struct DataParamsV {
 
 // Kernel launchers (gr_kernels.cu). Return cudaError_t as int.
 int launch_bitvector(const BvParams &p, void *stream);
-// armed cycle: p's out_released / out_cum / out_subcum / out_info are the ring BASES (slot 0);
-// the kernel polls desc->doorbell == seq for at most expire_ns and acknowledges in *ack
-int launch_bitvector_armed(const BvParams &p, const CycleDesc *desc, uint32_t seq, uint64_t expire_ns,
+// armed cycles: p's out_released / out_cum / out_subcum / out_info are the ring BASES (slot 0);
+// the kernel runs cycle seq, seq+1, ... as the host rings them (descriptor seq % 4), each awaited
+// for at most expire_ns, and acknowledges every cycle in *ack
+int launch_bitvector_armed(const BvParams &p, const CycleDesc *descs, uint32_t seq, uint64_t expire_ns,
                            uint32_t *ack, void *stream);
 int launch_bitvector_virtual(const BvParamsV &pv, void *stream);
 int launch_data_virtual(const DataParamsV &pv, int buffer_f16, int stats, void *stream);

@@ -370,6 +370,7 @@ __device__ __forceinline__ void bitvector_body(const BvParams &p, bool preloaded
         p.out_info->total_chunks = (status == ST_OK) ? run_ch : 0;
         p.out_info->total_subs = (status == ST_OK) ? s_tot[2] : 0;
         p.out_info->elems = (status == ST_OK) ? (int64_t)s_elems : 0;
+        asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(&p.out_info->tag), "r"(p.htag) : "memory");
         // a drain cycle is not awaited by the host: a failure (or a step left incomplete)
         // is reported through the error block checked by the next gr_step / gr_wait
         if (p.drain && (status != ST_OK || !complete)) {
@@ -385,80 +386,86 @@ __global__ void __launch_bounds__(NT, 1024 / NT) bitvector_kernel(const __grid_c
     bitvector_body<NT>(p);
 }
 
-// Armed cycle: launched right after a cycle, before the next one exists. Its threads poll the
-// pinned descriptor's LL words in parallel (thread i: word i) for at most `expire_ns` (bounded
-// residency: one small CTA; a device-wide synchronize waits at most that long), so the whole
-// cycle arrives in one PCIe round trip after the host writes it. Thread 0 owns the control word
-// and acknowledges in pinned memory: ack = seq << 1 | 1 "accepted, running this cycle", or
-// seq << 1 "expired before the doorbell" (the host then launches the cycle itself).
+// Armed cycles: a bitvector kernel that stays resident across a tight loop of cycles. For cycle
+// sq = seq, seq+1, ... its threads poll descriptor sq % GR_ARM_SLOTS (pinned host memory) in
+// parallel (thread i: LL word i) for at most `expire_ns` — bounded residency: one small CTA, and
+// a device-wide synchronize waits at most that long — so a cycle arrives in one PCIe round trip
+// after the host writes it. Thread 0 owns the control word and acknowledges every cycle in
+// pinned memory: ack = sq << 1 | 1 "accepted, running it", or sq << 1 "expired before its
+// doorbell" (the host then launches that cycle itself). While waiting, the kernel already holds
+// the step's released bits and the group records (the previous cycle ran in this very CTA).
 template <int NT>
 __global__ void __launch_bounds__(NT, 1024 / NT) bitvector_kernel_armed(const __grid_constant__ BvParams p,
-                                                                        const CycleDesc *desc, uint32_t seq,
+                                                                        const CycleDesc *descs, uint32_t seq,
                                                                         uint64_t expire_ns, uint32_t *ack) {
     __shared__ BvParams sp;
     __shared__ volatile int s_state;  // 0 polling, 1 run, 2 leave
     __shared__ uint32_t sv[16 + 2 * GR_BV_INLINE_WORDS];
     const int t = threadIdx.x;
     const bool mine = t < D_SLOT + 1 || (t >= D_BITS && t < D_BITS + p.W) || (t >= D_MARKED && t < D_MARKED + p.W);
-    if (t == 0) s_state = 0;
-    // the previous cycle's kernel finished before this one started (stream order): its released
-    // bits and the static group records can be loaded while the doorbell is still awaited
-    bitvector_preload(p);
-    __syncthreads();
-    if (t == 0) {
-        const uint64_t dl = globaltimer() + expire_ns;
-        for (;;) {
-            const uint64_t v = ld_acquire_sys64(&desc->w[D_CTRL]);
-            if ((uint32_t)(v >> 32) == seq) {
-                if (v & 1ull) { s_state = 2; break; }  // retired by the host
-                sv[D_CTRL] = (uint32_t)v;
-                st_relaxed_sys32(ack, (seq << 1) | 1u);
-                s_state = 1;
-                break;
-            }
-            if (globaltimer() > dl) {
-                st_relaxed_sys32(ack, seq << 1);
-                s_state = 2;
-                break;
-            }
-            __nanosleep(64);
-        }
-    } else if (mine) {  // data words: valid once they carry seq (written before the control word)
-        for (;;) {
-            const uint64_t v = ld_relaxed_sys64(&desc->w[t]);
-            if ((uint32_t)(v >> 32) == seq) { sv[t] = (uint32_t)v; break; }
-            if (s_state == 2) break;
-            __nanosleep(64);
-        }
-    }
-    {   // static part: copy the launch parameters word by word
+    {   // static part: copy the launch parameters word by word (once)
         const uint32_t *src = reinterpret_cast<const uint32_t *>(&p);
         uint32_t *dst = reinterpret_cast<uint32_t *>(&sp);
         for (int i = t; i < (int)(sizeof(BvParams) / 4); i += blockDim.x) dst[i] = src[i];
     }
-    __syncthreads();
-    if (s_state != 1) return;
-    for (int w = t; w < p.W; w += blockDim.x) {
-        sp.inline_bits[w] = sv[D_BITS + w];
-        sp.inline_marked[w] = sv[D_MARKED + w];
+    if (t == 0) st_relaxed_sys32(ack + 1, seq);  // resident: data kernels may now wait on its records
+    for (uint32_t sq = seq;; sq = (sq + 1 >= 0x7fffffffu) ? 1u : sq + 1) {
+        if (t == 0) s_state = 0;
+        // the previous cycle (this CTA's, or the kernel before it in the stream) is complete: its
+        // released bits and the static group records load while the doorbell is awaited
+        bitvector_preload(p);
+        __syncthreads();
+        const CycleDesc *desc = descs + sq % GR_ARM_SLOTS;
+        if (t == 0) {
+            const uint64_t dl = globaltimer() + expire_ns;
+            for (;;) {
+                const uint64_t v = ld_acquire_sys64(&desc->w[D_CTRL]);
+                if ((uint32_t)(v >> 32) == sq) {
+                    if (v & 1ull) { s_state = 2; break; }  // retired by the host
+                    st_relaxed_sys32(ack, (sq << 1) | 1u);
+                    s_state = 1;
+                    break;
+                }
+                if (globaltimer() > dl) {
+                    st_relaxed_sys32(ack, sq << 1);
+                    s_state = 2;
+                    break;
+                }
+                __nanosleep(64);
+            }
+        } else if (mine) {  // data words: valid once they carry sq (written before the control word)
+            for (;;) {
+                const uint64_t v = ld_relaxed_sys64(&desc->w[t]);
+                if ((uint32_t)(v >> 32) == sq) { sv[t] = (uint32_t)v; break; }
+                if (s_state == 2) break;
+                __nanosleep(64);
+            }
+        }
+        __syncthreads();
+        if (s_state != 1) return;
+        for (int w = t; w < p.W; w += blockDim.x) {
+            sp.inline_bits[w] = sv[D_BITS + w];
+            sp.inline_marked[w] = sv[D_MARKED + w];
+        }
+        if (t == 0) {
+            const int slot = (int)sv[D_SLOT];
+            sp.epoch = sv[D_EPOCH];
+            sp.tag = sv[D_TAG];
+            sp.htag = sv[D_HTAG];
+            sp.parity = (int32_t)sv[D_PARITY];
+            sp.new_step = (int32_t)sv[D_NEW_STEP];
+            sp.check_async = (int32_t)sv[D_CHECK_ASYNC];
+            sp.abort_flag = (int32_t)sv[D_ABORT];
+            sp.shutdown_flag = (int32_t)sv[D_SHUTDOWN];
+            sp.out_released = p.out_released + (size_t)slot * p.G;
+            sp.out_cum = p.out_cum + (size_t)slot * (p.G + 1);
+            sp.out_subcum = p.out_subcum + (size_t)slot * (p.G + 1);
+            sp.out_info = p.out_info + slot;
+        }
+        __syncthreads();
+        bitvector_body<NT>(sp, true);
+        __syncthreads();
     }
-    if (t == 0) {
-        const int slot = (int)sv[D_SLOT];
-        sp.epoch = sv[D_EPOCH];
-        sp.tag = sv[D_TAG];
-        sp.htag = sv[D_HTAG];
-        sp.parity = (int32_t)sv[D_PARITY];
-        sp.new_step = (int32_t)sv[D_NEW_STEP];
-        sp.check_async = (int32_t)sv[D_CHECK_ASYNC];
-        sp.abort_flag = (int32_t)sv[D_ABORT];
-        sp.shutdown_flag = (int32_t)sv[D_SHUTDOWN];
-        sp.out_released = p.out_released + (size_t)slot * p.G;
-        sp.out_cum = p.out_cum + (size_t)slot * (p.G + 1);
-        sp.out_subcum = p.out_subcum + (size_t)slot * (p.G + 1);
-        sp.out_info = p.out_info + slot;
-    }
-    __syncthreads();
-    bitvector_body<NT>(sp, true);
 }
 
 template <int NT>
@@ -499,13 +506,13 @@ int launch_bitvector(const BvParams &p, void *stream) {
     return (int)cudaGetLastError();
 }
 
-int launch_bitvector_armed(const BvParams &p, const CycleDesc *desc, uint32_t seq, uint64_t expire_ns,
+int launch_bitvector_armed(const BvParams &p, const CycleDesc *descs, uint32_t seq, uint64_t expire_ns,
                            uint32_t *ack, void *stream) {
     const size_t smem = bitvector_smem(p);
     static std::atomic<uint64_t> done{0};
     if (first_use_on_device(done))
         cudaFuncSetAttribute(bitvector_kernel_armed<BV_THREADS>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
-    bitvector_kernel_armed<BV_THREADS><<<1, BV_THREADS, smem, (cudaStream_t)stream>>>(p, desc, seq, expire_ns, ack);
+    bitvector_kernel_armed<BV_THREADS><<<1, BV_THREADS, smem, (cudaStream_t)stream>>>(p, descs, seq, expire_ns, ack);
     return (int)cudaGetLastError();
 }
 
@@ -743,6 +750,37 @@ __device__ __forceinline__ void grad_store1(char *g, int64_t idx, bool f16, floa
     else *reinterpret_cast<float *>(g + idx * 4) = x;
 }
 
+// Armed cycles: the data kernel is not ordered after the (resident) bitvector kernel by a stream
+// event; one thread per CTA waits until the cycle's record carries its tag. false = timed out.
+__device__ __forceinline__ bool wait_cycle_record(const DataParams &p) {
+    __shared__ int s_ok;
+    if (threadIdx.x == 0) {
+        int ok = 1;
+        if (p.wait_tag) {
+            const uint32_t *tagp = &p.info->tag;
+            uint32_t v;
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(tagp) : "memory");
+            if (v != p.wait_tag) {
+                const uint64_t dl = globaltimer() + p.timeout_ns;
+                for (;;) {
+                    __nanosleep(64);
+                    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(tagp) : "memory");
+                    if (v == p.wait_tag) break;
+                    if (globaltimer() > dl) {
+                        p.err->where = 3;
+                        p.err->code = ST_TIMEOUT;
+                        ok = 0;
+                        break;
+                    }
+                }
+            }
+        }
+        s_ok = ok;
+    }
+    __syncthreads();
+    return s_ok != 0;
+}
+
 // chunk id of item i of the released set (binary search over the cumulative counts)
 __device__ __forceinline__ int chunk_of_item(const DataParams &p, int nrel, int i) {
     int lo = 0, hi = nrel - 1;
@@ -773,6 +811,7 @@ template <typename BT, bool STATS>
 __global__ void __launch_bounds__(LC_THREADS, GR_LC_MINB) local_kernel(const __grid_constant__ DataParams p) {
     using B = Buf<BT>;
     constexpr int LCU = STATS ? GR_LC_STATS_UNROLL : LC_UNROLL;
+    if (!wait_cycle_record(p)) return;
     const int lane = threadIdx.x & 31;
     const int gw = blockIdx.x * (LC_THREADS / 32) + (threadIdx.x >> 5);
     const int nw = gridDim.x * (LC_THREADS / 32);
@@ -1172,6 +1211,15 @@ __device__ __forceinline__ void xfer_body(const DataParams &p, const int cta, co
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     }
     const int nst = p.nstages;
+    if (!wait_cycle_record(p)) {
+        __syncthreads();
+        if (tid == 0 && atomicAdd(p.done_counter, 1) == nctas - 1) {
+            *p.work_counter = 0;
+            *p.pack_counter = 0;
+            *p.done_counter = 0;
+        }
+        return;
+    }
     const int nrel = p.info->n_released;
     const int total = p.info->total_chunks;
     // algorithm chosen on the device from the released message size (same rule on every rank)

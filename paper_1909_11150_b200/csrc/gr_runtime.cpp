@@ -171,10 +171,13 @@ struct gr_ctx {
     gr::CycleDesc *h_desc = nullptr, *d_desc = nullptr;  // [kArmSlots], pinned + mapped
     uint32_t *h_ack = nullptr, *d_ack = nullptr;         // the armed kernel's acknowledgement
     bool arm_ok = false, armed = false;
-    uint32_t arm_seq = 0;
+    uint32_t arm_seq = 0, arm_first = 0;  // arm_first: the running armed kernel's first cycle
+    bool arm_resident = false;            // it has started (h_ack[1] == arm_first)
     int64_t arm_expire_us = 100, arm_gap_us = 50;  // kernel lifetime; arm only after gaps below this
+    int64_t arm_ring_delay_us = 0;  // testing (GR_ARM_RING_DELAY_US): host stall after the doorbell
     double last_gap_us = 1e30;                      // host time between the last two gr_step calls
-    std::chrono::steady_clock::time_point last_step_exit{}, arm_time{};
+    std::chrono::steady_clock::time_point last_step_exit{}, arm_time{};  // arm_time: the armed kernel
+    // polls cycle arm_seq with a deadline no earlier than arm_time + arm_expire_us
     int data_ctas[4] = {0, 0, 0, 0};       // world.comm_ctas (or every SM)
     int data_ctas_full[4] = {0, 0, 0, 0};  // every SM (drain cycles)
     int lag1 = -1, lag2 = -1;  // GR_LAG1 / GR_LAG2 overrides (tuning; -1 = default multiple of the grid)
@@ -637,6 +640,7 @@ int setup_local(gr_ctx *c) {
         c->arm_ok = !c->vg && c->W <= GR_BV_INLINE_WORDS && !(ae && atoi(ae) == 0);
         if (const char *x = getenv("GR_ARM_US")) c->arm_expire_us = std::max<int64_t>(1, atoll(x));
         if (const char *x = getenv("GR_ARM_GAP_US")) c->arm_gap_us = std::max<int64_t>(0, atoll(x));
+        if (const char *x = getenv("GR_ARM_RING_DELAY_US")) c->arm_ring_delay_us = std::max<int64_t>(0, atoll(x));
     }
 
     // 208 KB of dynamic shared memory per CTA: the stage ring, and with push the output tiles
@@ -771,17 +775,21 @@ void fill_bv_static(gr_ctx *c, gr::BvParams &p) {
     p.err = c->h_err;
 }
 
-// launch the next cycle's bitvector kernel now: it polls its descriptor's doorbell for at most
-// arm_expire_us. Only in tight cycle loops (the last gap between gr_step calls below
+static uint32_t next_seq(uint32_t s) { return s + 1 >= 0x7fffffffu ? 1u : s + 1; }  // ack carries seq << 1
+
+// launch a resident bitvector kernel for the coming cycles: it polls each cycle's descriptor for
+// at most arm_expire_us. Only in tight cycle loops (the last gap between gr_step calls below
 // arm_gap_us): a training loop that ticks every few hundred us never holds an SM for it.
 int arm(gr_ctx *c) {
     if (!c->arm_ok || c->armed || c->sticky || c->timing || c->last_gap_us > (double)c->arm_gap_us) return GR_OK;
-    if (++c->arm_seq >= 0x7fffffffu) c->arm_seq = 1;  // the acknowledgement carries seq << 1
-    gr::CycleDesc *d = c->d_desc + c->arm_seq % kArmSlots;
+    c->arm_seq = next_seq(c->arm_seq);
+    c->arm_first = c->arm_seq;
+    c->arm_resident = false;
     gr::BvParams p{};
     fill_bv_static(c, p);
     c->arm_time = std::chrono::steady_clock::now();  // its lifetime starts no earlier than this
-    int lrc = gr::launch_bitvector_armed(p, d, c->arm_seq, (uint64_t)c->arm_expire_us * 1000ull, c->d_ack, c->s_coord);
+    int lrc = gr::launch_bitvector_armed(p, c->d_desc, c->arm_seq, (uint64_t)c->arm_expire_us * 1000ull, c->d_ack,
+                                         c->s_coord);
     if (lrc) return fail(c, GR_ECUDA, "armed bitvector launch: %s", cudaGetErrorString((cudaError_t)lrc));
     c->armed = true;
     return GR_OK;
@@ -1365,27 +1373,58 @@ static int step_impl(gr_ctx *c, int32_t *released, gr_cycle_info *info, uint32_t
         hd->w[gr::D_ABORT] = sq | (uint32_t)p.abort_flag;
         hd->w[gr::D_SHUTDOWN] = sq | (uint32_t)p.shutdown_flag;
         hd->w[gr::D_SLOT] = sq | (uint32_t)slot;
+        // taken before the doorbell: the kernel's wait for the next cycle starts after it sees
+        // this one, so its deadline is no earlier than t_ring + arm_expire_us (host preemption
+        // between the doorbell and a later timestamp must not stretch the host's estimate)
+        const auto t_ring = std::chrono::steady_clock::now();
         __atomic_store_n(&hd->w[gr::D_CTRL], sq, __ATOMIC_RELEASE);
-        c->armed = false;
-        // rung well inside the kernel's lifetime (which starts after its launch): it cannot have
-        // expired, go on. Otherwise its acknowledgement tells: accepted, or expired before the
-        // doorbell (then this cycle is launched as usual).
+        if (c->arm_ring_delay_us)  // a preempted host: the kernel may run this cycle and expire on the next first
+            std::this_thread::sleep_for(std::chrono::microseconds(c->arm_ring_delay_us));
+        // rung well inside the kernel's lifetime for this cycle (which starts after its launch, or
+        // after the previous cycle was rung): it cannot have expired, go on. Otherwise its
+        // acknowledgement tells: accepted, or expired before the doorbell (then this cycle is
+        // launched as usual and a new kernel armed after it).
         const auto t0 = std::chrono::steady_clock::now();
         const double since = std::chrono::duration<double, std::micro>(t0 - c->arm_time).count();
         uint32_t a = 1u;
+        bool gone_after = false;  // accepted, and it has since expired waiting for the next cycle
         if (since > (double)c->arm_expire_us * 0.8 - 10.0) {
-            const uint32_t want = c->arm_seq << 1;
-            while (((a = __atomic_load_n(c->h_ack, __ATOMIC_ACQUIRE)) & ~1u) != want) {
+            // the ack word holds the kernel's latest decision: (seq << 1) | accepted. It can be
+            // past this cycle already (accepted it, ran it, then expired on the next one).
+            const uint32_t s0 = c->arm_seq, s1 = next_seq(s0);
+            for (;;) {
+                a = __atomic_load_n(c->h_ack, __ATOMIC_ACQUIRE);
+                if ((a >> 1) == s0) break;
+                if ((a >> 1) == s1) {
+                    a = 1u;
+                    gone_after = true;
+                    break;
+                }
                 if (std::chrono::steady_clock::now() - t0 > std::chrono::milliseconds(c->world.timeout_ms + 5000))
                     return fail(c, GR_ETIMEOUT, "armed bitvector kernel never acknowledged");
             }
+            c->arm_resident = true;
         }
-        if (a & 1u) {
+        if ((a & 1u) && !c->arm_resident) {
+            // the data kernel below spins until this cycle's record carries its tag: that is only
+            // safe with the bitvector kernel already on an SM (it started, so it stays resident),
+            // never with it queued behind SMs the spinning data CTAs could occupy
+            while (__atomic_load_n(c->h_ack + 1, __ATOMIC_ACQUIRE) != c->arm_first) {
+                if (std::chrono::steady_clock::now() - t0 > std::chrono::milliseconds(c->world.timeout_ms + 5000))
+                    return fail(c, GR_ETIMEOUT, "armed bitvector kernel never started");
+            }
+            c->arm_resident = true;
+        }
+        if (a & 1u) {  // accepted: the same kernel then waits for the next cycle
             ran_armed = true;
             c->stats.armed_cycles++;
-        } else {
+            c->arm_seq = next_seq(c->arm_seq);
+            c->arm_time = t_ring;
+            if (gone_after) c->armed = false;  // arm() below queues a new one
+        } else {           // expired: the cycle's marks are in p.inline_* for the launch below
+            c->armed = false;
             c->stats.armed_expired++;
-        }  // else expired: the cycle's marks are in p.inline_* for the launch below
+        }
     }
     if (ran_armed) {
     } else if (c->vg) {
@@ -1483,8 +1522,13 @@ static int step_impl(gr_ctx *c, int32_t *released, gr_cycle_info *info, uint32_t
         d.lag2 = c->lag2 >= 0 ? c->lag2 : 8 * ctas;
         if (d.lag2 <= d.lag1) d.lag2 = d.lag1 + ctas;  // one override against the other's default
         d.lagd = c->lagd >= 0 ? c->lagd : 2 * ctas;
-        CK(c, cudaEventRecord(c->ev_bv, c->s_coord));
-        CK(c, cudaStreamWaitEvent(c->s_data, c->ev_bv, 0));
+        if (ran_armed) {  // the bitvector kernel stays resident: the data kernel waits for its tag
+            d.wait_tag = p.htag;
+        } else {
+            d.wait_tag = 0;
+            CK(c, cudaEventRecord(c->ev_bv, c->s_coord));
+            CK(c, cudaStreamWaitEvent(c->s_data, c->ev_bv, 0));
+        }
         std::pair<cudaEvent_t, cudaEvent_t> evd{};
         if (c->timing) {
             evd = get_ev_pair(c);

@@ -321,6 +321,19 @@ def test_multi_gpu_cfg1(n):
     assert _torchrun(n, "--suite", "cfg1", "--seeds", "0:30") == 0
 
 
+@pytest.mark.parametrize("n", [2, 4])
+def test_multi_gpu_armed(n):
+    """Armed cycles at N>1 (gr.h gr_step): every gap qualifies, so one resident bitvector kernel
+    per rank serves cycle after cycle and each data kernel waits for its cycle's record; then
+    with the host stalled after each doorbell (the kernel runs ahead and expires unseen)."""
+    if gpu_count() < n:
+        pytest.skip(f"needs {n} GPUs")
+    on = {"GR_ARM": "1", "GR_ARM_GAP_US": "1000000000", "GR_ARM_US": "1000000"}
+    assert _torchrun(n, "--suite", "cfg1", "--seeds", "40:50", env_extra=on) == 0
+    late = dict(on, GR_ARM_US="100", GR_ARM_RING_DELAY_US="300")
+    assert _torchrun(n, "--suite", "cfg1", "--seeds", "50:54", env_extra=late) == 0
+
+
 @pytest.mark.parametrize("n", [2, 4, 8])
 def test_multi_gpu_edge(n):
     if gpu_count() < n:
@@ -441,7 +454,7 @@ def test_new_gradient_buffers_every_step_async_wait(gpu):
     ctx.gr_finalize()
 
 
-@pytest.mark.parametrize("arm", ["on", "expire", "off"])
+@pytest.mark.parametrize("arm", ["on", "expire", "off", "late"])
 def test_armed_cycles_n1(gpu, arm, monkeypatch):
     """Armed cycles (gr.h gr_step): in a tight cycle loop the next cycle's bitvector kernel is
     launched ahead of the cycle and polls a pinned doorbell; gr_wait / gr_step_drain / timing
@@ -449,13 +462,17 @@ def test_armed_cycles_n1(gpu, arm, monkeypatch):
     normal launch. Many-cycle cfg1 schedules (host marks, drains with host or stream-ordered
     marks, a blocking gr_wait per step, timing mode toggled) stay bit-exact against the oracle
     with the armed path always taken ("on": every gap qualifies, the kernel lives 1 s), always
-    expiring ("expire": 1 us lifetime), and off."""
+    expiring ("expire": 1 us lifetime), off, and "late": a 100 us lifetime with the host stalled
+    300 us after every doorbell, so the resident kernel runs the cycle and expires on the next
+    one before the host reads its acknowledgement (the ack word is already one cycle ahead)."""
     import torch
     from paper_1909_11150_b200 import GR_F16, Context
     from tests.parity_lib import run_case_on_rank, run_drain_case_on_rank
     monkeypatch.setenv("GR_ARM", "0" if arm == "off" else "1")
     monkeypatch.setenv("GR_ARM_GAP_US", "1000000000")
-    monkeypatch.setenv("GR_ARM_US", "1" if arm == "expire" else "1000000")
+    monkeypatch.setenv("GR_ARM_US", {"expire": "1", "late": "100"}.get(arm, "1000000"))
+    if arm == "late":
+        monkeypatch.setenv("GR_ARM_RING_DELAY_US", "300")
     base = cfg1_case(11)
     ctx = Context(rank=0, world_size=1, device=0, numel=base.numel, group_of=base.group_of, buffer_dtype=GR_F16,
                   timeout_ms=10000)
@@ -475,6 +492,8 @@ def test_armed_cycles_n1(gpu, arm, monkeypatch):
             assert 0 < st.armed_cycles < st.cycles and st.armed_expired == 0
         elif arm == "expire":  # a 1 us lifetime: most armed kernels expire, a few are rung in time
             assert st.armed_expired > 0 and st.armed_cycles + st.armed_expired < st.cycles
+        elif arm == "late":  # each armed kernel that is rung runs that cycle, then expires unseen
+            assert st.armed_cycles > 0
         else:
             assert st.armed_cycles == 0 and st.armed_expired == 0
     finally:
