@@ -163,10 +163,10 @@ int gr_mark_ready_async(gr_ctx *ctx, int32_t rank, int32_t tensor_id, void *dev_
 
 /* gr_step — COLLECTIVE: one coordination cycle ("tic").
  * Runs the bitvector kernel. In a tight cycle loop (less than GR_ARM_GAP_US = 50 us between
- * gr_step calls) it is already running: one resident kernel serves cycle after cycle, polling a
- * pinned "doorbell" for at most GR_ARM_US = 100 us per cycle; gr_step writes the cycle's marks
- * and rings it, and the cycle's data kernel waits for the record it writes — no launch on the
- * critical path (an expired kernel acknowledges and the cycle is launched as usual; gr_wait,
+ * gr_step calls) it is already running, polling a pinned "doorbell" for at most GR_ARM_US =
+ * 100 us per cycle; gr_step writes the cycle's marks and rings it. At N = 1 one resident kernel
+ * serves cycle after cycle and the cycle's data kernel waits for the record it writes; at N > 1
+ * each armed kernel serves one cycle and gr_step arms the next — no launch on the critical path (an expired kernel acknowledges and the cycle is launched as usual; gr_wait,
  * gr_step_drain and timing mode retire it; GR_ARM=0 turns this off; a device-wide synchronize
  * waits at most GR_ARM_US for it).
  * The kernel does: populate (a thread per word from the host

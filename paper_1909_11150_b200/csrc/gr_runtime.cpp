@@ -1405,7 +1405,7 @@ static int step_impl(gr_ctx *c, int32_t *released, gr_cycle_info *info, uint32_t
             }
             c->arm_resident = true;
         }
-        if ((a & 1u) && !c->arm_resident) {
+        if ((a & 1u) && !c->arm_resident && c->N == 1) {
             // the data kernel below spins until this cycle's record carries its tag: that is only
             // safe with the bitvector kernel already on an SM (it started, so it stays resident),
             // never with it queued behind SMs the spinning data CTAs could occupy
@@ -1420,7 +1420,7 @@ static int step_impl(gr_ctx *c, int32_t *released, gr_cycle_info *info, uint32_t
             c->stats.armed_cycles++;
             c->arm_seq = next_seq(c->arm_seq);
             c->arm_time = t_ring;
-            if (gone_after) c->armed = false;  // arm() below queues a new one
+            if (gone_after || c->N > 1) c->armed = false;  // arm() below queues a new one (N > 1: one cycle each)
         } else {           // expired: the cycle's marks are in p.inline_* for the launch below
             c->armed = false;
             c->stats.armed_expired++;
@@ -1522,7 +1522,7 @@ static int step_impl(gr_ctx *c, int32_t *released, gr_cycle_info *info, uint32_t
         d.lag2 = c->lag2 >= 0 ? c->lag2 : 8 * ctas;
         if (d.lag2 <= d.lag1) d.lag2 = d.lag1 + ctas;  // one override against the other's default
         d.lagd = c->lagd >= 0 ? c->lagd : 2 * ctas;
-        if (ran_armed) {  // the bitvector kernel stays resident: the data kernel waits for its tag
+        if (ran_armed && c->N == 1) {  // the bitvector kernel stays resident: the data kernel waits for its tag
             d.wait_tag = p.htag;
         } else {
             d.wait_tag = 0;
