@@ -290,6 +290,8 @@ void debug_dump(gr_ctx *c) {
 int device_error(gr_ctx *c) {
     const int code = c->h_err->code, where = c->h_err->where;
     if (code == 3) debug_dump(c);
+    if (code == 3 && where == 3)  // wait_cycle_record: the resident bitvector kernel never wrote the record
+        return fail(c, GR_ETIMEOUT, "reduction timed out waiting for its cycle's record (armed bitvector kernel)");
     if (code == 3)
         return fail(c, GR_ETIMEOUT, "reduction timed out waiting for a peer (%s flag)", where == 1 ? "pack" : "reduce-scatter");
     if (code >= 10) {
