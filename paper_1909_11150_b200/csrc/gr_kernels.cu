@@ -386,7 +386,8 @@ __global__ void __launch_bounds__(NT, 1024 / NT) bitvector_kernel(const __grid_c
     bitvector_body<NT>(p);
 }
 
-// Armed cycles: a bitvector kernel that stays resident across a tight loop of cycles. For cycle
+// Armed cycles: a bitvector kernel that stays resident across a tight loop of cycles (N = 1; at
+// N > 1 it serves one cycle and exits). For cycle
 // sq = seq, seq+1, ... its threads poll descriptor sq % GR_ARM_SLOTS (pinned host memory) in
 // parallel (thread i: LL word i) for at most `expire_ns` — bounded residency: one small CTA, and
 // a device-wide synchronize waits at most that long — so a cycle arrives in one PCIe round trip
